@@ -6,10 +6,3 @@ this package is its thin ctypes binding (``api``) plus the seeded input generato
 there is no CPU fallback.
 """
 from . import synth  # noqa: F401  (no native dependency)
-
-
-def __getattr__(name):
-    if name == "api":
-        from . import api as _api
-        return _api
-    raise AttributeError(name)

@@ -1,0 +1,343 @@
+// msd_api.cu -- the C ABI of libmsd (declared and documented in include/msd.h):
+// argument validation, workspace carving and kernel launches.  No arithmetic of
+// the method lives here.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "msd_common.cuh"
+#include "msd_internal.h"
+
+using namespace msd;
+
+namespace {
+
+thread_local std::string g_err;
+
+msd_status fail(msd_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+msd_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(MSD_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+msd_status check_arch() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    static int cached[64];
+    static std::once_flag once[64];
+    if (dev < 0 || dev >= 64) return fail(MSD_E_ARCH, "device index %d", dev);
+    std::call_once(once[dev], [&]() {
+        int major = 0, minor = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cached[dev] = major * 10 + minor;
+    });
+    if (cached[dev] != 100)
+        return fail(MSD_E_ARCH, "libmsd is built for sm_100a (B200); device %d is sm_%d", dev,
+                    cached[dev]);
+    return MSD_OK;
+}
+
+double env_double(const char* name, double dflt) {
+    const char* v = getenv(name);
+    return v ? atof(v) : dflt;
+}
+
+// ----------------------------------------------------------------- profiling
+struct Prof {
+    std::mutex mu;
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+    int32_t total_launches = 0;
+} g_prof;
+
+std::pair<cudaEvent_t, cudaEvent_t> prof_pair() {
+    std::pair<cudaEvent_t, cudaEvent_t> p;
+    if (!g_prof.pool.empty()) {
+        p = g_prof.pool.back();
+        g_prof.pool.pop_back();
+    } else {
+        cudaEventCreate(&p.first);
+        cudaEventCreate(&p.second);
+    }
+    return p;
+}
+
+struct Engine {
+    LevelDesc lv;
+    int32_t L, B, K;
+    int64_t V;
+    int32_t bf16;
+    const int32_t* cand0;
+    const int32_t* m0;
+    const float* u_acc;
+    const float* u_emit;
+    int64_t ua_l, ua_b, ue_l, ue_b;
+    int32_t greedy, ibonus, fbonus, draft_fed;
+    int32_t *n_acc, *m_cand, *out_tok, *out_len, *rollback;
+    int32_t out_ld;
+    float *pos_dtv, *pos_kl;
+    msd_pair_stats* stats;
+    uint32_t* flags;
+    void* ws;
+    size_t ws_bytes;
+    cudaStream_t stream;
+};
+
+msd_status validate_levels(const msd_logits* lv, int32_t L, int32_t K, int64_t V, int32_t ibonus,
+                           int32_t extra_rows_needed, int32_t* bf16) {
+    const int32_t dt = lv[0].dtype;
+    if (dt != MSD_F32 && dt != MSD_BF16) return fail(MSD_E_DTYPE, "unknown dtype %d", dt);
+    const int64_t es = dt == MSD_BF16 ? 2 : 4;
+    for (int l = 0; l < L; ++l) {
+        if (lv[l].dtype != dt) return fail(MSD_E_DTYPE, "level %d dtype differs from level 0", l);
+        if (!lv[l].ptr) return fail(MSD_E_ARG, "level %d ptr is NULL", l);
+        if (lv[l].ld < V) return fail(MSD_E_ARG, "level %d ld=%lld < V=%lld", l, (long long)lv[l].ld, (long long)V);
+        int32_t need = l == 0 ? K : (extra_rows_needed >= 0 ? K + extra_rows_needed : (ibonus ? K + l : K + 1));
+        if (lv[l].rows < need) return fail(MSD_E_ARG, "level %d has %d rows, needs >= %d", l, lv[l].rows, need);
+        if (lv[l].batch_stride < (int64_t)lv[l].rows * lv[l].ld)
+            return fail(MSD_E_ARG, "level %d batch_stride < rows*ld", l);
+        if (((uintptr_t)lv[l].ptr) % 16 || (lv[l].ld * es) % 16 || (lv[l].batch_stride * es) % 16)
+            return fail(MSD_E_ALIGN, "level %d rows are not 16-byte aligned (ptr, ld*elem, batch_stride*elem)", l);
+    }
+    *bf16 = dt == MSD_BF16;
+    return MSD_OK;
+}
+
+msd_status run_engine(const Engine& E) {
+    if (E.B == 0) return MSD_OK;
+    const WsLayout w = ws_layout(E.L, E.B, E.K, E.V);
+    if (!E.ws || E.ws_bytes < w.total)
+        return fail(MSD_E_WORKSPACE, "workspace %zu bytes < required %zu", E.ws_bytes, w.total);
+    if (((uintptr_t)E.ws) % 256) return fail(MSD_E_WORKSPACE, "workspace must be 256-byte aligned");
+    char* ws = reinterpret_cast<char*>(E.ws);
+
+    CoreParams cp;
+    memset(&cp, 0, sizeof(cp));
+    cp.lv = E.lv;
+    cp.L = E.L; cp.B = E.B; cp.K = E.K; cp.V = E.V;
+    cp.C = w.C; cp.U = w.U;
+    cp.n_items = (int64_t)w.U * w.C;
+    cp.partials = reinterpret_cast<Partial*>(ws + w.partials);
+    cp.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
+    cp.kl = reinterpret_cast<double*>(ws + w.kl);
+    cp.resid = reinterpret_cast<double*>(ws + w.resid);
+    cp.cnt = reinterpret_cast<uint32_t*>(ws + w.cnt);
+    cp.ready = reinterpret_cast<uint32_t*>(ws + w.ready);
+    cp.flags = E.flags;
+    cp.err = reinterpret_cast<uint32_t*>(ws + w.hdr);
+
+    TailParams tp;
+    memset(&tp, 0, sizeof(tp));
+    tp.lv = E.lv;
+    tp.L = E.L; tp.B = E.B; tp.K = E.K; tp.C = w.C; tp.V = E.V;
+    tp.cand0 = E.cand0; tp.m0 = E.m0;
+    tp.u_acc = E.u_acc; tp.u_emit = E.u_emit;
+    tp.ua_l = E.ua_l; tp.ua_b = E.ua_b; tp.ue_l = E.ue_l; tp.ue_b = E.ue_b;
+    tp.greedy = E.greedy; tp.ibonus = E.ibonus; tp.fbonus = E.fbonus; tp.draft_fed = E.draft_fed;
+    tp.n_acc = E.n_acc; tp.m_cand = E.m_cand; tp.out_tok = E.out_tok; tp.out_ld = E.out_ld;
+    tp.out_len = E.out_len; tp.rollback = E.rollback;
+    tp.pos_dtv = E.pos_dtv; tp.pos_kl = E.pos_kl; tp.stats = E.stats; tp.flags = E.flags;
+    tp.partials = cp.partials; tp.rowstat = cp.rowstat; tp.kl = cp.kl; tp.resid = cp.resid;
+    tp.cnt = cp.cnt; tp.ready = cp.ready;
+    tp.z_safe = env_double("MSD_Z_SAFE", 0.05);
+    tp.exact_all = (int32_t)env_double("MSD_EXACT_DRAWS", 0.0);
+
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    {
+        std::lock_guard<std::mutex> g(g_prof.mu);
+        if (g_prof.on) {
+            ev = prof_pair();
+            cudaEventRecord(ev.first, E.stream);
+        }
+        g_prof.total_launches += 2;
+    }
+    cudaError_t e = launch_core(cp, E.bf16, E.greedy, E.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "msd_core launch");
+    if (ev.first) {
+        std::lock_guard<std::mutex> g(g_prof.mu);
+        cudaEventRecord(ev.second, E.stream);
+        g_prof.pending.push_back(ev);
+    }
+    e = launch_tail(tp, E.bf16, E.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "msd_tail launch");
+    return MSD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* msd_last_error(void) { return g_err.c_str(); }
+int32_t msd_abi_version(void) { return MSD_ABI_VERSION; }
+
+size_t msd_chain_verify_workspace(int32_t L, int32_t B, int32_t K, int64_t V) {
+    if (L < 2 || L > MAXL || B < 0 || K < 1 || V < 1) return 0;
+    return ws_layout(L, B, K, V).total;
+}
+size_t msd_verify_level_workspace(int32_t B, int32_t K, int64_t V) {
+    return msd_chain_verify_workspace(2, B, K, V);
+}
+
+msd_status msd_chain_verify(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                            const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                            int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                            int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                            int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                            msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                            void* stream) {
+    if (!levels) return fail(MSD_E_ARG, "levels is NULL");
+    if (L < 2 || L > MAXL) return fail(MSD_E_ARG, "L=%d outside [2,%d]", L, MAXL);
+    if (B < 0 || K < 1 || K + L > MAXC) return fail(MSD_E_ARG, "bad B=%d / K=%d (need K+L <= 32)", B, K);
+    if (V < 1 || V > (int64_t)128 * VS) return fail(MSD_E_ARG, "V=%lld outside [1, 524288]", (long long)V);
+    if (mode != MSD_STOCHASTIC && mode != MSD_GREEDY) return fail(MSD_E_ARG, "unknown mode %d", mode);
+    if (draft_fed < 0 || draft_fed > K) return fail(MSD_E_ARG, "draft_fed=%d outside [0,K]", draft_fed);
+    if (B == 0) return MSD_OK;
+    if (!draft_tok || !commit_tok || !commit_len || !flags || !n_acc)
+        return fail(MSD_E_ARG, "draft_tok, n_acc, commit_tok, commit_len and flags are required");
+    if (mode == MSD_STOCHASTIC && (!u_acc || !u_emit))
+        return fail(MSD_E_ARG, "u_acc / u_emit are required in stochastic mode");
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    Engine E;
+    memset(&E, 0, sizeof(E));
+    st = validate_levels(levels, L, K, V, intermediate_bonus, -1, &E.bf16);
+    if (st != MSD_OK) return st;
+    for (int l = 0; l < L; ++l) {
+        E.lv.ptr[l] = levels[l].ptr;
+        E.lv.ld[l] = levels[l].ld;
+        E.lv.bs[l] = levels[l].batch_stride;
+        E.lv.rows[l] = levels[l].rows;
+    }
+    E.L = L; E.B = B; E.K = K; E.V = V;
+    E.cand0 = draft_tok; E.m0 = nullptr;
+    E.u_acc = u_acc; E.u_emit = u_emit;
+    const int64_t W = K + L - 1;
+    E.ua_l = (int64_t)B * W; E.ua_b = W; E.ue_l = (int64_t)B * W; E.ue_b = W;
+    E.greedy = mode == MSD_GREEDY; E.ibonus = intermediate_bonus ? 1 : 0; E.fbonus = 1;
+    E.draft_fed = draft_fed;
+    E.n_acc = n_acc; E.m_cand = m_cand; E.out_tok = commit_tok; E.out_ld = (int32_t)W;
+    E.out_len = commit_len; E.rollback = rollback;
+    E.pos_dtv = pos_dtv; E.pos_kl = pos_kl; E.stats = stats; E.flags = flags;
+    E.ws = ws; E.ws_bytes = ws_bytes;
+    E.stream = reinterpret_cast<cudaStream_t>(stream);
+    return run_engine(E);
+}
+
+msd_status msd_verify_level(msd_logits q, msd_logits p, int32_t B, int32_t K, int64_t V,
+                            const int32_t* cand, const int32_t* m,
+                            const float* u_acc, const float* u_emit,
+                            int32_t mode, int32_t emit_bonus,
+                            int32_t* n_acc, int32_t* out_tok, int32_t* out_len,
+                            float* pos_dtv, float* pos_kl, msd_pair_stats* stats,
+                            uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
+    if (B < 0 || K < 1 || K + 2 > MAXC) return fail(MSD_E_ARG, "bad B=%d / K=%d (need K <= 30)", B, K);
+    if (V < 1 || V > (int64_t)128 * VS) return fail(MSD_E_ARG, "V=%lld outside [1, 524288]", (long long)V);
+    if (mode != MSD_STOCHASTIC && mode != MSD_GREEDY) return fail(MSD_E_ARG, "unknown mode %d", mode);
+    if (B == 0) return MSD_OK;
+    if (!cand || !out_tok || !out_len || !flags || !n_acc)
+        return fail(MSD_E_ARG, "cand, n_acc, out_tok, out_len and flags are required");
+    if (mode == MSD_STOCHASTIC && (!u_acc || !u_emit))
+        return fail(MSD_E_ARG, "u_acc / u_emit are required in stochastic mode");
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    msd_logits lv[2] = {q, p};
+    Engine E;
+    memset(&E, 0, sizeof(E));
+    st = validate_levels(lv, 2, K, V, 1, emit_bonus ? 1 : 0, &E.bf16);
+    if (st != MSD_OK) return st;
+    for (int l = 0; l < 2; ++l) {
+        E.lv.ptr[l] = lv[l].ptr;
+        E.lv.ld[l] = lv[l].ld;
+        E.lv.bs[l] = lv[l].batch_stride;
+        E.lv.rows[l] = lv[l].rows;
+    }
+    E.L = 2; E.B = B; E.K = K; E.V = V;
+    E.cand0 = cand; E.m0 = m;
+    E.u_acc = u_acc; E.u_emit = u_emit;
+    E.ua_l = 0; E.ua_b = K; E.ue_l = 0; E.ue_b = K + 1;
+    E.greedy = mode == MSD_GREEDY; E.ibonus = 0; E.fbonus = emit_bonus ? 1 : 0;
+    E.draft_fed = 0;
+    E.n_acc = n_acc; E.m_cand = nullptr; E.out_tok = out_tok; E.out_ld = K + 1;
+    E.out_len = out_len; E.rollback = nullptr;
+    E.pos_dtv = pos_dtv; E.pos_kl = pos_kl; E.stats = stats; E.flags = flags;
+    E.ws = ws; E.ws_bytes = ws_bytes;
+    E.stream = reinterpret_cast<cudaStream_t>(stream);
+    return run_engine(E);
+}
+
+msd_status msd_kv_rollback(const msd_paged_kv* kv, int32_t n_models, int32_t B,
+                           const int32_t* rollback, uint32_t* flags, void* stream) {
+    if (!kv || n_models < 0 || B < 0) return fail(MSD_E_ARG, "bad kv / n_models / B");
+    if (n_models == 0 || B == 0) return MSD_OK;
+    if (!rollback || !flags) return fail(MSD_E_ARG, "rollback and flags are required");
+    for (int i = 0; i < n_models; ++i) {
+        const msd_paged_kv& k = kv[i];
+        if (!k.seq_len || !k.block_table || !k.free_ids || !k.free_count)
+            return fail(MSD_E_ARG, "model %d: seq_len, block_table, free_ids, free_count required", i);
+        if (k.block_size < 1 || k.max_blocks < 0 || k.free_cap < 0)
+            return fail(MSD_E_ARG, "model %d: bad block_size / max_blocks / free_cap", i);
+        if (k.cache_mask && k.mask_ld < 1) return fail(MSD_E_ARG, "model %d: mask_ld < 1", i);
+    }
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    for (int m0 = 0; m0 < n_models; m0 += 8) {
+        RollbackParams p;
+        memset(&p, 0, sizeof(p));
+        p.n_models = n_models - m0 < 8 ? n_models - m0 : 8;
+        for (int i = 0; i < p.n_models; ++i) p.kv[i] = kv[m0 + i];
+        p.B = B;
+        p.rollback = rollback + (size_t)m0 * B;
+        p.flags = flags;
+        {
+            std::lock_guard<std::mutex> g(g_prof.mu);
+            g_prof.total_launches += 1;
+        }
+        cudaError_t e = launch_rollback(p, reinterpret_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "msd_rollback launch");
+    }
+    return MSD_OK;
+}
+
+msd_status msd_prof_enable(int32_t on) {
+    std::lock_guard<std::mutex> g(g_prof.mu);
+    g_prof.on = on != 0;
+    return MSD_OK;
+}
+
+msd_status msd_prof_read(double* core_ms, int32_t* core_launches, int32_t* total_launches) {
+    std::lock_guard<std::mutex> g(g_prof.mu);
+    double tot = 0.0;
+    for (auto& pr : g_prof.pending) {
+        cudaError_t e = cudaEventSynchronize(pr.second);
+        if (e != cudaSuccess) return cuda_fail(e, "msd_prof_read");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.first, pr.second);
+        tot += ms;
+        g_prof.pool.push_back(pr);
+    }
+    if (core_ms) *core_ms = tot;
+    if (core_launches) *core_launches = (int32_t)g_prof.pending.size();
+    if (total_launches) *total_launches = g_prof.total_launches;
+    g_prof.pending.clear();
+    g_prof.total_launches = 0;
+    return MSD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,245 @@
+// msd_common.cuh -- shared device helpers of libmsd (sm_100a only).
+//
+// Tiling used by every kernel: a "slice" is VS = T * ET consecutive vocabulary
+// entries of one logit row; thread t of a T-thread CTA owns the elements
+// (j * T + t) * VEC + k (j < ET/VEC, k < VEC) of the slice, i.e. 16-byte vectors
+// with the warp covering 512 contiguous bytes per access (conflict-free LDS.128,
+// fully coalesced LDG.128).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/msd.h"
+
+namespace msd {
+
+constexpr int T = 256;             // threads per CTA (core and tail)
+constexpr int NWARP = T / 32;
+constexpr int ET = 16;             // elements per thread per row per slice
+constexpr int VS = T * ET;         // slice length (4096 vocabulary entries)
+constexpr int MAXL = 4;            // chain levels supported
+constexpr int MAXC = 32;           // candidate slots (K + L - 1 <= 31)
+constexpr float NEG_CLAMP = -1e30f;  // logits are clamped to >= this (NaN kept)
+constexpr float NEG_MASKED = -1e29f; // clamped logits <= this mean "-inf" (p = 0)
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr double KL_INF_THRESH = 1e20;
+
+// Per (unit, level, slice) pass-1 record, published for the cross-CTA exchange.
+struct Partial {
+    float m;        // slice max (after the -1e30 clamp)
+    int32_t amax;   // first index (global vocab id) attaining m in the slice
+    double S;       // sum_v exp(z_v - m) over the slice
+    double Kl;      // sum_v exp(z_v - m) * (z_v - z'_v), z' = previous level's row
+};
+
+// Per (unit, level) result written by the combining CTA.
+struct RowStat {
+    double M;       // row max
+    double S;       // sum_v exp(z_v - M)
+    double lse;     // M + log S   (Eq. 1 normaliser)
+    int32_t amax;   // argmax, lowest id on ties
+    int32_t bad;    // NaN / +inf present or row all -inf
+};
+
+// Workspace layout (bytes), shared by host and device code.
+struct WsLayout {
+    size_t hdr, cnt, ready, partials, rowstat, kl, resid, total;
+    int32_t U, C, L;
+};
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline WsLayout ws_layout(int32_t L, int32_t B, int32_t K, int64_t V) {
+    WsLayout w;
+    w.L = L;
+    w.U = B * K;
+    w.C = (int32_t)ceil_div(V, VS);
+    size_t off = 0;
+    w.hdr = off;      off += 256;
+    w.cnt = off;      off = align_up(off + sizeof(uint32_t) * (size_t)w.U, 256);
+    w.ready = off;    off = align_up(off + sizeof(uint32_t) * (size_t)w.U, 256);
+    w.partials = off; off = align_up(off + sizeof(Partial) * (size_t)w.U * L * w.C, 256);
+    w.rowstat = off;  off = align_up(off + sizeof(RowStat) * (size_t)w.U * L, 256);
+    w.kl = off;       off = align_up(off + sizeof(double) * (size_t)w.U * (L - 1), 256);
+    w.resid = off;    off = align_up(off + sizeof(double) * (size_t)w.U * (L - 1) * w.C, 256);
+    w.total = off;
+    return w;
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ float ex2f(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ uint32_t max_nan_bf16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ float max_nan_f32(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t r;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(r));
+    return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+        "%2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 0.0;" : "=l"(p));
+    return p;
+}
+
+// ------------------------------------------------------------------ element access
+template <typename Tin>
+struct Elem;
+template <>
+struct Elem<float> {
+    static constexpr int VEC = 4;
+    __device__ static inline float load1(const float* p) { return __ldg(p); }
+};
+template <>
+struct Elem<__nv_bfloat16> {
+    static constexpr int VEC = 8;
+    __device__ static inline float load1(const __nv_bfloat16* p) {
+        return __bfloat162float(__ldg(p));
+    }
+};
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Unpack one 16-byte vector into VEC floats with the NaN-propagating -1e30 clamp.
+template <typename Tin>
+__device__ __forceinline__ void unpack_clamped(const uint4& v, float* x);
+template <>
+__device__ __forceinline__ void unpack_clamped<__nv_bfloat16>(const uint4& v, float* x) {
+    // -1e30 as bf16x2 pair: 0xF149 (bf16 of -1e30 rounds to -9.98e29)
+    const uint32_t c = 0xF149F149u;
+    uint32_t a = max_nan_bf16x2(v.x, c), b = max_nan_bf16x2(v.y, c);
+    uint32_t d = max_nan_bf16x2(v.z, c), e = max_nan_bf16x2(v.w, c);
+    x[0] = bf16lo(a); x[1] = bf16hi(a); x[2] = bf16lo(b); x[3] = bf16hi(b);
+    x[4] = bf16lo(d); x[5] = bf16hi(d); x[6] = bf16lo(e); x[7] = bf16hi(e);
+}
+template <>
+__device__ __forceinline__ void unpack_clamped<float>(const uint4& v, float* x) {
+    x[0] = max_nan_f32(__uint_as_float(v.x), NEG_CLAMP);
+    x[1] = max_nan_f32(__uint_as_float(v.y), NEG_CLAMP);
+    x[2] = max_nan_f32(__uint_as_float(v.z), NEG_CLAMP);
+    x[3] = max_nan_f32(__uint_as_float(v.w), NEG_CLAMP);
+}
+
+__device__ __forceinline__ float clamp1(float z) { return max_nan_f32(z, NEG_CLAMP); }
+
+// ------------------------------------------------------------------ warp reductions
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ int warp_min_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Combine C slice partials of one row into its RowStat (fixed order -> every CTA
+// that does it gets bit-identical results).  Executed by one full warp.
+__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out) {
+    const int lane = threadIdx.x & 31;
+    float m = -INFINITY;
+    for (int s = lane; s < C; s += 32) m = fmaxf(m, __ldcg(&parts[s].m));
+    m = warp_max(m);
+    double S = 0.0, Kl = 0.0;
+    int am = 0x7fffffff;
+    bool bad = false;
+    for (int s = lane; s < C; s += 32) {
+        float ms = __ldcg(&parts[s].m);
+        double Ss = __ldcg(&parts[s].S);
+        double Ks = __ldcg(&parts[s].Kl);
+        double f = exp((double)ms - (double)m);
+        S += Ss * f;
+        Kl += Ks * f;
+        if (ms == m) am = min(am, __ldcg(&parts[s].amax));
+        if (isnan(ms) || isnan(Ss)) bad = true;
+    }
+    S = warp_sum_d(S);
+    Kl = warp_sum_d(Kl);
+    am = warp_min_i(am);
+    bad = __any_sync(0xffffffffu, bad);
+    RowStat r;
+    r.M = (double)m;
+    r.S = S;
+    r.lse = (double)m + log(S);
+    r.amax = am == 0x7fffffff ? 0 : am;
+    r.bad = (bad || !(m > NEG_MASKED) || !isfinite(S) || !(m < INFINITY)) ? 1 : 0;
+    if (K_out) *K_out = Kl;
+    return r;
+}
+
+}  // namespace msd

@@ -1,0 +1,80 @@
+// msd_internal.h -- host-side launch interfaces between the C ABI (msd_api.cpp)
+// and the kernels.  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/msd.h"
+
+namespace msd {
+
+struct Partial;
+struct RowStat;
+
+struct LevelDesc {
+    const void* ptr[4];
+    int64_t ld[4];
+    int64_t bs[4];
+    int32_t rows[4];
+};
+
+struct CoreParams {
+    LevelDesc lv;
+    int32_t L, B, K, C, U;
+    int64_t V;
+    int64_t n_items;
+    int32_t stages;
+    Partial* partials;
+    RowStat* rowstat;
+    double* kl;
+    double* resid;
+    uint32_t* cnt;
+    uint32_t* ready;
+    uint32_t* flags;
+    uint32_t* err;
+};
+
+struct TailParams {
+    LevelDesc lv;
+    int32_t L, B, K, C;
+    int64_t V;
+    const int32_t* cand0;
+    const int32_t* m0;
+    const float* u_acc;
+    const float* u_emit;
+    int64_t ua_l, ua_b, ue_l, ue_b;
+    int32_t greedy, ibonus, fbonus, draft_fed;
+    int32_t* n_acc;
+    int32_t* m_cand;
+    int32_t* out_tok;
+    int32_t out_ld;
+    int32_t* out_len;
+    int32_t* rollback;
+    float* pos_dtv;
+    float* pos_kl;
+    msd_pair_stats* stats;
+    uint32_t* flags;
+    const Partial* partials;
+    const RowStat* rowstat;
+    const double* kl;
+    const double* resid;
+    uint32_t* cnt;
+    uint32_t* ready;
+    double z_safe;
+    int32_t exact_all;
+};
+
+struct RollbackParams {
+    msd_paged_kv kv[8];
+    int32_t n_models, B;
+    const int32_t* rollback;
+    uint32_t* flags;
+};
+
+// Returns cudaSuccess or the launch error.  bf16 = 1 for bf16 logits, 0 for f32.
+cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s);
+cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s);
+cudaError_t launch_rollback(const RollbackParams& p, cudaStream_t s);
+
+}  // namespace msd
