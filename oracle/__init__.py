@@ -54,7 +54,7 @@ def lib() -> ctypes.CDLL:
         L.or_sample_residual.argtypes = [P, d, P, d, i64, d, P, P]
         L.or_chain_verify.restype = ctypes.c_int
         L.or_chain_verify.argtypes = [P, i32, i32, i32, i64, P, P, P, P, i64, i64,
-                                      i32, i32, i32, i32, d,
+                                      i32, i32, i32, i32, d, d,
                                       P, P, P, i32, P, P, P, P, P, P, i32]
         L.or_rollback_mask.restype = None
         L.or_rollback_mask.argtypes = [P, i32, i32, P, P, P]
@@ -145,7 +145,7 @@ class _Level(ctypes.Structure):
 
 def chain_verify(levels, cand0, u_acc=None, u_emit=None, *, m0=None, greedy=False,
                  intermediate_bonus=True, final_bonus=True, draft_fed=None,
-                 tie_eps=1e-6, nthreads=0):
+                 tie_eps=1e-6, tie_eps_draw=None, nthreads=0):
     """Run the whole cascade for every request.
 
     levels: list of L arrays [B, rows_l, V] (any float dtype; converted exactly to f64).
@@ -183,6 +183,7 @@ def chain_verify(levels, cand0, u_acc=None, u_emit=None, *, m0=None, greedy=Fals
         lv, L, B, K, V, _p(cand0), _p(m0a), _p(u_acc), _p(u_emit), B * W, W,
         int(greedy), int(intermediate_bonus), int(final_bonus),
         int(K - 1 if draft_fed is None else draft_fed), float(tie_eps),
+        float(tie_eps if tie_eps_draw is None else tie_eps_draw),
         _p(o["n_acc"]), _p(o["m_cand"]), _p(o["out_tok"]), out_ld, _p(o["out_len"]),
         _p(o["rollback"]), _p(o["pos_dtv"]), _p(o["pos_kl"]), _p(o["near_tie"]),
         _p(o["flags"]), int(nthreads))

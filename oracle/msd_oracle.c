@@ -76,7 +76,8 @@ double or_kl(const double* za, double A, const double* zb, double B, int64_t V) 
  * exp(log p(t) - log q(t)).  q(t) = 0: accept iff p(t) > 0.
  * near_tie is set when |u - min(1,p/q)| < tie_eps (caller passes the eps via the
  * global below; reading R18). */
-static double g_tie_eps = 1e-6;
+static double g_tie_eps = 1e-6;       /* acceptance band (north star: |u - p/q| < 1e-6) */
+static double g_tie_eps_draw = 1e-6;  /* inverse-CDF band |u - C/Z| (reading R18) */
 int or_accept(double za_t, double A, double zb_t, double B, double u, int* near_tie) {
     if (za_t == -INFINITY) {               /* p(t) = 0: never accepted (u >= 0) */
         if (near_tie && u < g_tie_eps) *near_tie = 1;
@@ -103,7 +104,7 @@ static int64_t inv_cdf(const double* w, int64_t V, double Z, double u, int* near
         ns_add(&c, w[t]);
         double ct = ns_get(&c);
         if (ct > target && w[t] > 0.0) {
-            if (near_tie && (fabs(u - prev / Z) < g_tie_eps || fabs(u - ct / Z) < g_tie_eps))
+            if (near_tie && (fabs(u - prev / Z) < g_tie_eps_draw || fabs(u - ct / Z) < g_tie_eps_draw))
                 *near_tie = 1;
             return t;
         }
@@ -296,13 +297,14 @@ int or_chain_verify(const or_level* lv, int32_t L, int32_t B, int32_t K, int64_t
                     const int32_t* cand0, const int32_t* m0,
                     const float* u_acc, const float* u_emit, int64_t u_lstride, int64_t u_bstride,
                     int32_t greedy, int32_t intermediate_bonus, int32_t final_bonus,
-                    int32_t draft_fed, double tie_eps,
+                    int32_t draft_fed, double tie_eps, double tie_eps_draw,
                     int32_t* n_acc, int32_t* m_cand, int32_t* out_tok, int32_t out_ld,
                     int32_t* out_len, int32_t* rollback, double* pos_dtv, double* pos_kl,
                     int32_t* near_tie, uint32_t* flags, int32_t nthreads) {
     if (L < 2 || B < 0 || K < 1 || V < 1 || !lv || !cand0) return 1;
     if (!greedy && (!u_acc || !u_emit)) return 1;
     g_tie_eps = tie_eps > 0 ? tie_eps : 1e-6;
+    g_tie_eps_draw = tie_eps_draw > 0 ? tie_eps_draw : g_tie_eps;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #pragma omp parallel for schedule(dynamic, 1)

@@ -57,7 +57,9 @@ int64_t or_sample_residual(const double* za, double A, const double* zb, double 
  *   rollback[l*B+b]                          per-model KV rollback r_b (model l = level l)
  *   pos_dtv/pos_kl[((l-1)*B+b)*K + i]        divergence of pair (l-1,l) at draft position i < K
  *   near_tie[b]                              first level (1-based verifier index l) whose decision
- *                                            was a near tie (|u - threshold| < tie_eps), else 0
+ *                                            was a near tie, else 0: acceptance |u - min(1,p/q)| <
+ *                                            tie_eps, draws |u - C/Z| < tie_eps_draw (C = a CDF
+ *                                            boundary adjacent to the drawn token)
  *   flags[b]                                 OR_F_* bits
  * Returns 0 on success, nonzero on argument error.
  */
@@ -65,7 +67,7 @@ int or_chain_verify(const or_level* lv, int32_t L, int32_t B, int32_t K, int64_t
                     const int32_t* cand0, const int32_t* m0,
                     const float* u_acc, const float* u_emit, int64_t u_lstride, int64_t u_bstride,
                     int32_t greedy, int32_t intermediate_bonus, int32_t final_bonus,
-                    int32_t draft_fed, double tie_eps,
+                    int32_t draft_fed, double tie_eps, double tie_eps_draw,
                     int32_t* n_acc, int32_t* m_cand, int32_t* out_tok, int32_t out_ld,
                     int32_t* out_len, int32_t* rollback, double* pos_dtv, double* pos_kl,
                     int32_t* near_tie, uint32_t* flags, int32_t nthreads);

@@ -5,6 +5,8 @@ import torch
 import oracle
 
 DIV_REL, DIV_ABS = 1e-4, 1e-7     # DESIGN.md R18
+ACCEPT_BAND = 1e-6                # north star: |u - p/q| < 1e-6
+DRAW_BAND = 1e-7                  # inverse-CDF draws: |u - C/Z| < 1e-7 (tighter than R18's 1e-6)
 
 
 def to_np(o):
@@ -12,7 +14,7 @@ def to_np(o):
 
 
 def run_oracle(inp, *, greedy=False, intermediate_bonus=True, draft_fed=None, requests=None,
-               nthreads=0):
+               nthreads=0, tie_eps_draw=DRAW_BAND):
     """Oracle on (a subset of) the requests of a synth.ChainInputs."""
     sel = slice(None) if requests is None else requests
     levels = [t[sel].float().cpu().numpy() if t.dtype != torch.float32 else t[sel].cpu().numpy()
@@ -23,7 +25,7 @@ def run_oracle(inp, *, greedy=False, intermediate_bonus=True, draft_fed=None, re
     ue = inp.u_emit[:, sel].cpu().numpy()
     return oracle.chain_verify(levels, draft, ua, ue, greedy=greedy,
                                intermediate_bonus=intermediate_bonus, draft_fed=draft_fed,
-                               nthreads=nthreads)
+                               tie_eps=ACCEPT_BAND, tie_eps_draw=tie_eps_draw, nthreads=nthreads)
 
 
 def compare(gpu, ref, requests=None, check_rollback=True):
@@ -58,11 +60,11 @@ def compare(gpu, ref, requests=None, check_rollback=True):
     return rep
 
 
-def assert_parity(gpu, ref, requests=None, check_rollback=True, max_near_tie_frac=0.05):
+def assert_parity(gpu, ref, requests=None, check_rollback=True, max_near_tie_frac=0.1):
     rep = compare(gpu, ref, requests, check_rollback)
     assert not rep["mismatch"], f"token/length mismatch outside near ties: requests {rep['mismatch'][:20]}"
     assert rep["dtv_err"] <= 0, f"DTV outside tolerance by {rep['dtv_err']}"
     assert rep["kl_err"] <= 0, f"KL outside tolerance by {rep['kl_err']}"
     n = ref["out_len"].shape[0]
-    assert rep["near_tie"] <= max(1, max_near_tie_frac * n), rep
+    assert rep["near_tie"] <= max(2, max_near_tie_frac * n), rep
     return rep
