@@ -126,12 +126,15 @@ __global__ void __launch_bounds__(T, 2) core_kernel(CoreParams p) {
             const float wm = warp_max(tm);
             wm_r[l] = wm;
             float sum = 0.f, ks = 0.f;
+            // KL numerator relative to the shift s_w = m_w,l - m_w,l-1 (restored in float64
+            // at the combine) so the dominant term does not sit in the fp32 accumulator.
+            const float shift = l > 0 ? wm - wm_r[l > 0 ? l - 1 : 0] : 0.f;
 #pragma unroll
             for (int k = 0; k < ET; ++k) {
                 const float ev = ex2f((x[k] - wm) * LOG2E);
                 e[l][k] = ev;
                 sum += ev;
-                if (l > 0) ks = fmaf(ev, x[k] - xprev[k], ks);
+                if (l > 0) ks = fmaf(ev, (x[k] - xprev[k]) - shift, ks);
             }
             sum = warp_sum(sum);
             if (l > 0) ks = warp_sum(ks);
@@ -165,7 +168,9 @@ __global__ void __launch_bounds__(T, 2) core_kernel(CoreParams p) {
             double f = act ? exp((double)mw - (double)ms) : 0.0;
             if (!(mw > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;  // fully masked warp
             double Ss = act ? (double)w_S[l][wi] * f : 0.0;
-            double Ks = act ? (double)w_K[l][wi] * f : 0.0;
+            double Ks = 0.0;
+            if (act && l > 0 && f != 0.0)
+                Ks = ((double)w_K[l][wi] + ((double)mw - (double)w_m[l - 1][wi]) * (double)w_S[l][wi]) * f;
             int am = (act && mw == ms) ? w_am[l][wi] : 0x7fffffff;
 #pragma unroll
             for (int o = 4; o > 0; o >>= 1) {
