@@ -1,177 +1,385 @@
 // msd_core.cu -- the streaming pass over every logit row at the draft positions.
 //
 // Rows a1 (Eq. 1 normaliser) and a5 (Eq. 5 DTV; KL) of the
-// hot path, for all L chain levels at once so that every logit byte is read from
-// HBM exactly once.
+// hot path, for all L chain levels at once so every logit byte is read from HBM
+// exactly once.
 //
-// Work decomposition.  A *unit* is one (request b, draft position i < K); it owns
-// the L rows Z_l[b, i, :] (one per level).  A unit is cut into C slices of VS = 4096
-// vocabulary entries; an *item* is (unit, slice).  The kernel is persistent and
-// cooperative: CTA g processes items g, g+G, g+2G, ... in order, so the C items of
-// a unit run concurrently on C different CTAs (G >= C => no deadlock).
+// Decomposition.  A *unit* is one (request b, draft position i < K) and owns the L
+// rows Z_l[b, i, :].  A unit is cut into C slices of VS = 4096 vocabulary entries;
+// an *item* is (unit, slice).  The kernel is persistent and cooperative (one CTA per
+// SM): CTA g processes items g, g+G, g+2G, ...; the C items of a unit run
+// concurrently on C CTAs, which exchange per-slice partials through global memory.
 //
-// Per item:
-//   1. TMA (cp.async.bulk) streams the L row slices into a S-stage shared-memory
-//      ring; thread 0 keeps S items in flight per CTA.
-//   2. pass 1 (registers): per warp, e_v = 2^((z_v - m_w) log2 e) relative to the
-//      warp max m_w (one MUFU.EX2 per element), sum S_w and the KL numerator
-//      K_w = sum e_v (z_v - z'_v) against the previous level's row.  The e_v stay in
-//      registers for pass 2 (no second exp, no second read).
-//   3. warp 0 folds the 8 warp records into the slice partial (m_s, S_s, K_s, argmax)
-//      and publishes it; the CTA that publishes the unit's last slice combines the C
-//      partials (fixed order, float64) into the unit's row stats and releases them.
-//   4. pass 2 (registers): with M_l, S_l known, the residual mass of each adjacent
-//      pair in this slice, R_s = sum_v max(p_v - q_v, 0) (= its DTV share, and the
-//      per-slice CDF the tail's residual draw needs), evaluated as
-//      max(e_a - rho e_b, 0) with rho = c_b S_a / (S_b c_a) split into hi+lo floats.
+// Warp specialisation (12 warps):
+//   warps 0-7  compute: pass 1 of item j  -- slice max (named barrier among compute
+//                warps), e_v = 2^((z_v - m_s) log2 e) (one MUFU.EX2 per element), sums S
+//                and the KL numerator, e_v parked in TMEM (tcgen05.st);
+//              then pass 2 of item j-LAG -- e_v back from TMEM (tcgen05.ld), residual
+//                mass of each adjacent pair  sum_v max(p_v - q_v, 0)  in this slice.
+//   warp 8     producer: TMA bulk copies (cp.async.bulk) of the L row slices into an
+//                S-stage shared-memory ring.
+//   warp 9     publisher: folds the compute warps' records into the slice partial,
+//                publishes it, and -- when it is the unit's last slice -- combines the
+//                C partials (float64, fixed order) into the unit's row statistics.
+//   warp 10    fetcher: waits until an item's unit statistics are released and turns
+//                them into the pass-2 factors of that slice (float64).
+//   warp 11    reducer: sums the pass-2 warp records into the slice residual R_s.
+// The exchange latency is hidden behind LAG items of pass 1 (TMEM holds LAG+1 items
+// of exponentials per compute thread: 256 columns / (16 L)).
 #include "msd_common.cuh"
 #include "msd_internal.h"
 
 namespace msd {
 
+constexpr int NCW = 8;                 // compute warps
+constexpr int CT = NCW * 32;           // compute threads (the slice mapping uses CT == T)
+constexpr int CORE_THREADS = CT + 4 * 32;
+constexpr int W_PROD = 8, W_PUB = 9, W_FETCH = 10, W_RED = 11;
+constexpr int SMAX = 6;
+constexpr int NRMAX = 8;
+static_assert(CT == T, "slice mapping assumes 256 compute threads");
+
+struct Rec1 {
+    float S, K;
+    int am;
+    float pad;
+};
+struct RowF {               // pass-2 factors of one row of the current slice
+    float rho_hi, rho_lo;   // rho = c_b S_a / (S_b c_a) for the pair ending at this row
+    double scale;           // c_a / S_a
+    int skip;               // c_a == 0: the slice carries no mass of this row
+    int pad;
+};
+template <int L>
+struct Ctl {
+    uint64_t full[SMAX], empty[SMAX];
+    uint64_t rec1_full[NRMAX], rowf_full[NRMAX], rowf_empty[NRMAX], rec2_full[NRMAX], rec2_empty[NRMAX];
+    uint32_t taddr;
+    float wmax[2][L][NWARP];
+    float ms[NRMAX][L];
+    Rec1 rec1[NRMAX][L][NWARP];
+    RowF rowf[NRMAX][L];
+    double rec2[NRMAX][L][NWARP];
+    double rec2_scale[NRMAX][L];
+    int rec2_skip[NRMAX][L];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t* p, uint32_t v) {
+    uint32_t r;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+
+__device__ __forceinline__ void tm_st16(uint32_t ta, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+        : "r"(ta)
+        : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t clamp_bf16x2(uint32_t w) { return max_nan_bf16x2(w, 0xF149F149u); }
+
 template <typename Tin, int L, bool GREEDY>
-__global__ void __launch_bounds__(T, 2) core_kernel(CoreParams p) {
+__global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NV = ET / VEC;
     constexpr int ES = (int)sizeof(Tin);
+    constexpr int NR = 256 / (16 * L);      // TMEM item slots per compute thread
+    constexpr int LAG = NR - 1;
+    static_assert(NR <= NRMAX && NR >= 2, "TMEM slots");
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = p.stages;
     Tin* ring = reinterpret_cast<Tin*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * L * VS * ES);
-
-    __shared__ float w_m[L][NWARP];
-    __shared__ float w_S[L][NWARP];
-    __shared__ float w_K[L][NWARP];
-    __shared__ int w_am[L][NWARP];
-    __shared__ double w_R[L][NWARP];
-    __shared__ RowStat s_row[L];
-    __shared__ double s_K[L];
-    __shared__ int s_last;
+    Ctl<L>& c = *reinterpret_cast<Ctl<L>*>(smem + align_up((size_t)S * L * VS * ES, 128));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t G = gridDim.x;
     const int64_t n_my = p.n_items > (int64_t)blockIdx.x ? (p.n_items - blockIdx.x + G - 1) / G : 0;
-    const uint64_t pol = policy_evict_first();
+    const int C = p.C;
 
-    if (tid == 0) {
-        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    auto issue = [&](int64_t j) {
-        const int64_t w = blockIdx.x + j * G;
-        const int64_t u = w / p.C;
-        const int s = (int)(w % p.C);
-        const int64_t b = u / p.K, i = u % p.K;
-        const int st = (int)(j % S);
-        const int64_t len = min((int64_t)VS, p.V - (int64_t)s * VS);
-        const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
-        mbar_arrive_expect_tx(&full[st], bytes * L);
-        if (bytes) {
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
-                                 i * p.lv.ld[l] + (int64_t)s * VS;
-                bulk_g2s(ring + ((size_t)st * L + l) * VS, src, bytes, &full[st], pol);
+    if (warp == W_PROD) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], NCW); }
+            for (int q = 0; q < NR; ++q) {
+                mbar_init(&c.rec1_full[q], NCW);
+                mbar_init(&c.rowf_full[q], 1);
+                mbar_init(&c.rowf_empty[q], NCW);
+                mbar_init(&c.rec2_full[q], NCW);
+                mbar_init(&c.rec2_empty[q], 1);
             }
+            fence_mbar_init();
         }
+        __syncwarp();
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&c.taddr)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    auto item = [&](int64_t j, int64_t& u, int& s, int64_t& b, int64_t& i) {
+        const int64_t w = blockIdx.x + j * G;
+        u = w / C;
+        s = (int)(w % C);
+        b = u / p.K;
+        i = u % p.K;
     };
 
-    if (tid == 0)
-        for (int64_t j = 0; j < S && j < n_my; ++j) issue(j);
-
-    for (int64_t j = 0; j < n_my; ++j) {
-        const int64_t w = blockIdx.x + j * G;
-        const int64_t u = w / p.C;
-        const int s = (int)(w % p.C);
-        const int64_t b = u / p.K, i = u % p.K;
-        const int st = (int)(j % S);
-        const int64_t base = (int64_t)s * VS;
-        const int len = (int)min((int64_t)VS, p.V - base);
-        const int len_bulk = (len * ES) / 16 * 16 / ES;
-
-        mbar_wait(&full[st], (uint32_t)((j / S) & 1));
-
-        // ---------------- pass 1
-        float e[L][ET];
-        float xprev[ET];
-        float wm_r[L];
+    if (warp < NCW) {
+        // ================================================================ compute warps
+        const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
+        for (int64_t j = 0; j < n_my + LAG; ++j) {
+            if (j < n_my) {
+                int64_t u, b, i;
+                int s;
+                item(j, u, s, b, i);
+                const int st = (int)(j % S);
+                const int q = (int)(j % NR);
+                const int64_t base = (int64_t)s * VS;
+                const int len = (int)min((int64_t)VS, p.V - base);
+                const int len_bulk = (len * ES) / 16 * 16 / ES;
+                mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
+                // ---- raw rows -> registers (clamped), warp max per row
+                uint4 raw[L][NV];
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-            float x[ET];
-            const Tin* sl = ring + ((size_t)st * L + l) * VS;
+                for (int l = 0; l < L; ++l) {
+                    const Tin* sl = ring + ((size_t)st * L + l) * VS;
 #pragma unroll
-            for (int jv = 0; jv < NV; ++jv) {
-                const int e0 = (jv * T + tid) * VEC;
-                if (e0 + VEC <= len_bulk) {
-                    uint4 v = *reinterpret_cast<const uint4*>(sl + e0);
-                    unpack_clamped<Tin>(v, &x[jv * VEC]);
-                } else {
-                    const Tin* g = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
-                                   i * p.lv.ld[l] + base;
+                    for (int jv = 0; jv < NV; ++jv) {
+                        const int e0 = (jv * T + tid) * VEC;
+                        if (e0 + VEC <= len_bulk) {
+                            raw[l][jv] = *reinterpret_cast<const uint4*>(sl + e0);
+                        } else {   // ragged end of the row: element-wise from smem / global
+                            const Tin* g = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
+                                           i * p.lv.ld[l] + base;
+                            Tin xs[VEC];
 #pragma unroll
-                    for (int k = 0; k < VEC; ++k) {
-                        const int ee = e0 + k;
-                        float z = NEG_CLAMP;
-                        if (ee < len_bulk) z = clamp1((float)sl[ee]);
-                        else if (ee < len) z = clamp1(Elem<Tin>::load1(g + ee));
-                        x[jv * VEC + k] = z;
+                            for (int k = 0; k < VEC; ++k) {
+                                const int ee = e0 + k;
+                                Tin z = (Tin)(-INFINITY);
+                                if (ee < len_bulk) z = sl[ee];
+                                else if (ee < len) z = g[ee];
+                                xs[k] = z;
+                            }
+                            raw[l][jv] = *reinterpret_cast<const uint4*>(xs);
+                        }
+                    }
+                }
+                float msl[L];
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    float tm = -INFINITY;
+                    if (ES == 2) {
+                        uint32_t mx = 0xFF80FF80u;  // (-inf, -inf)
+#pragma unroll
+                        for (int jv = 0; jv < NV; ++jv) {
+                            raw[l][jv].x = clamp_bf16x2(raw[l][jv].x);
+                            raw[l][jv].y = clamp_bf16x2(raw[l][jv].y);
+                            raw[l][jv].z = clamp_bf16x2(raw[l][jv].z);
+                            raw[l][jv].w = clamp_bf16x2(raw[l][jv].w);
+                            mx = max_nan_bf16x2(mx, max_nan_bf16x2(max_nan_bf16x2(raw[l][jv].x, raw[l][jv].y),
+                                                                   max_nan_bf16x2(raw[l][jv].z, raw[l][jv].w)));
+                        }
+                        tm = fmaxf(bf16lo(mx), bf16hi(mx));
+                    } else {
+#pragma unroll
+                        for (int jv = 0; jv < NV; ++jv) {
+                            float xs[4];
+                            unpack_clamped<float>(raw[l][jv], xs);
+                            raw[l][jv] = make_uint4(__float_as_uint(xs[0]), __float_as_uint(xs[1]),
+                                                    __float_as_uint(xs[2]), __float_as_uint(xs[3]));
+                            tm = fmaxf(tm, fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])));
+                        }
+                    }
+                    tm = warp_max(tm);
+                    if (lane == 0) c.wmax[j & 1][l][warp] = tm;
+                }
+                bar_compute();
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    float m = lane < NWARP ? c.wmax[j & 1][l][lane] : -INFINITY;
+#pragma unroll
+                    for (int o = 4; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    msl[l] = __shfl_sync(0xffffffffu, m, 0);
+                }
+                if (warp == 0 && lane == 0) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) c.ms[q][l] = msl[l];
+                }
+                // ---- exponentials relative to the slice max, sums, TMEM park
+                float xprev[ET];
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    float x[ET];
+#pragma unroll
+                    for (int jv = 0; jv < NV; ++jv) {
+                        const uint4 r = raw[l][jv];
+                        if (ES == 2) {
+                            x[jv * 8 + 0] = bf16lo(r.x); x[jv * 8 + 1] = bf16hi(r.x);
+                            x[jv * 8 + 2] = bf16lo(r.y); x[jv * 8 + 3] = bf16hi(r.y);
+                            x[jv * 8 + 4] = bf16lo(r.z); x[jv * 8 + 5] = bf16hi(r.z);
+                            x[jv * 8 + 6] = bf16lo(r.w); x[jv * 8 + 7] = bf16hi(r.w);
+                        } else {
+                            x[(jv * 4 + 0) % ET] = __uint_as_float(r.x); x[(jv * 4 + 1) % ET] = __uint_as_float(r.y);
+                            x[(jv * 4 + 2) % ET] = __uint_as_float(r.z); x[(jv * 4 + 3) % ET] = __uint_as_float(r.w);
+                        }
+                    }
+                    const float m = msl[l];
+                    const float shift = l > 0 ? m - msl[l > 0 ? l - 1 : 0] : 0.f;
+                    float e[ET];
+                    float sum = 0.f, ks = 0.f;
+#pragma unroll
+                    for (int k = 0; k < ET; ++k) {
+                        e[k] = ex2f((x[k] - m) * LOG2E);
+                        sum += e[k];
+                        if (l > 0) ks = fmaf(e[k], (x[k] - xprev[k]) - shift, ks);
+                    }
+                    tm_st16(tbase + (uint32_t)(q * 16 * L + l * 16), e);
+                    sum = warp_sum(sum);
+                    if (l > 0) ks = warp_sum(ks);
+                    int am = 0x7fffffff;
+                    if (GREEDY) {
+#pragma unroll
+                        for (int k = ET - 1; k >= 0; --k)
+                            if (x[k] == m) am = (int)(base + ((k / VEC) * T + tid) * VEC + (k % VEC));
+                        am = warp_min_i(am);
+                    }
+                    if (lane == 0) {
+                        Rec1 r;
+                        r.S = sum; r.K = ks; r.am = am; r.pad = 0.f;
+                        c.rec1[q][l][warp] = r;
+                    }
+#pragma unroll
+                    for (int k = 0; k < ET; ++k) xprev[k] = x[k];
+                }
+                tm_wait_st();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&c.empty[st]);
+                    mbar_arrive(&c.rec1_full[q]);
+                }
+            }
+            if (j >= LAG) {
+                // ---- pass 2 of item j2 = j - LAG
+                const int64_t j2 = j - LAG;
+                const int q2 = (int)(j2 % NR);
+                mbar_wait(&c.rowf_full[q2], (uint32_t)((j2 / NR) & 1));
+                RowF f[L];
+#pragma unroll
+                for (int l = 0; l < L; ++l) f[l] = c.rowf[q2][l];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&c.rowf_empty[q2]);
+                float ev[L][ET];
+#pragma unroll
+                for (int l = 0; l < L; ++l) tm_ld16(tbase + (uint32_t)(q2 * 16 * L + l * 16), ev[l]);
+                tm_wait_ld();
+                float acc[L];
+#pragma unroll
+                for (int l = 1; l < L; ++l) {
+                    float a = 0.f;
+                    if (!f[l].skip) {
+                        const float rh = f[l].rho_hi, rl = f[l].rho_lo;
+#pragma unroll
+                        for (int k = 0; k < ET; ++k) {
+                            float t = fmaf(-ev[l - 1][k], rh, ev[l][k]);
+                            t = fmaf(-ev[l - 1][k], rl, t);
+                            a += fmaxf(t, 0.f);
+                        }
+                    }
+                    acc[l] = warp_sum(a);
+                }
+                if (j2 >= NR) mbar_wait(&c.rec2_empty[q2], (uint32_t)(((j2 / NR) - 1) & 1));
+                if (lane == 0) {
+#pragma unroll
+                    for (int l = 1; l < L; ++l) c.rec2[q2][l][warp] = (double)acc[l];
+                    if (warp == 0) {
+#pragma unroll
+                        for (int l = 1; l < L; ++l) {
+                            c.rec2_scale[q2][l] = f[l].scale;
+                            c.rec2_skip[q2][l] = f[l].skip;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&c.rec2_full[q2]);
+            }
+        }
+    } else if (warp == W_PROD) {
+        // ================================================================ TMA producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            for (int64_t j = 0; j < n_my; ++j) {
+                const int st = (int)(j % S);
+                if (j >= S) mbar_wait(&c.empty[st], (uint32_t)(((j / S) - 1) & 1));
+                int64_t u, b, i;
+                int s;
+                item(j, u, s, b, i);
+                const int64_t len = min((int64_t)VS, p.V - (int64_t)s * VS);
+                const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
+                mbar_arrive_expect_tx(&c.full[st], bytes * L);
+                if (bytes) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
+                                         i * p.lv.ld[l] + (int64_t)s * VS;
+                        bulk_g2s(ring + ((size_t)st * L + l) * VS, src, bytes, &c.full[st], pol);
                     }
                 }
             }
-            float tm = x[0];
-#pragma unroll
-            for (int k = 1; k < ET; ++k) tm = fmaxf(tm, x[k]);
-            const float wm = warp_max(tm);
-            wm_r[l] = wm;
-            float sum = 0.f, ks = 0.f;
-            // KL numerator relative to the shift s_w = m_w,l - m_w,l-1 (restored in float64
-            // at the combine) so the dominant term does not sit in the fp32 accumulator.
-            const float shift = l > 0 ? wm - wm_r[l > 0 ? l - 1 : 0] : 0.f;
-#pragma unroll
-            for (int k = 0; k < ET; ++k) {
-                const float ev = ex2f((x[k] - wm) * LOG2E);
-                e[l][k] = ev;
-                sum += ev;
-                if (l > 0) ks = fmaf(ev, (x[k] - xprev[k]) - shift, ks);
-            }
-            sum = warp_sum(sum);
-            if (l > 0) ks = warp_sum(ks);
-            int am = 0x7fffffff;
-            if (GREEDY) {
-#pragma unroll
-                for (int k = ET - 1; k >= 0; --k)
-                    if (x[k] == wm) am = (int)(base + ((k / VEC) * T + tid) * VEC + (k % VEC));
-                am = warp_min_i(am);
-            }
-            if (lane == 0) {
-                w_m[l][warp] = wm;
-                w_S[l][warp] = sum;
-                w_K[l][warp] = ks;
-                w_am[l][warp] = am;
-            }
-#pragma unroll
-            for (int k = 0; k < ET; ++k) xprev[k] = x[k];
         }
-        __syncthreads();  // B1: stage `st` fully consumed, warp records visible
-        if (tid == 0 && j + S < n_my) issue(j + S);
-
-        // ---------------- slice partials -> publish -> unit combine
-        if (warp == 0) {
+    } else if (warp == W_PUB) {
+        // ================================================================ publisher / combiner
+        int64_t prev_u = -1;
+        uint32_t prev_old = 0;
+        auto combine_unit = [&](int64_t u) {
+            __threadfence();
+            RowStat rs[L];
+            double Kl[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) rs[l] = combine_row(p.partials + ((size_t)u * L + l) * C, C, &Kl[l]);
+            if (lane == 0) {
+                bool bad = false;
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    p.rowstat[(size_t)u * L + l] = rs[l];
+                    bad |= rs[l].bad != 0;
+                }
+#pragma unroll
+                for (int l = 1; l < L; ++l)
+                    p.kl[(size_t)u * (L - 1) + (l - 1)] = Kl[l] / rs[l].S - (rs[l].lse - rs[l - 1].lse);
+                if (bad) atomicOr(&p.flags[u / p.K], (uint32_t)MSD_F_NONFINITE);
+                __threadfence();
+                st_release_u32(&p.ready[u], 1u);
+            }
+            __syncwarp();
+        };
+        for (int64_t j = 0; j < n_my; ++j) {
+            int64_t u, b, i;
+            int s;
+            item(j, u, s, b, i);
+            const int q = (int)(j % NR);
+            mbar_wait(&c.rec1_full[q], (uint32_t)((j / NR) & 1));
             const int l = lane >> 3, wi = lane & 7;
             const bool act = l < L;
-            const float mw = act ? w_m[l][wi] : -INFINITY;
-            float ms = mw;
-#pragma unroll
-            for (int o = 4; o > 0; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-            double f = act ? exp((double)mw - (double)ms) : 0.0;
-            if (!(mw > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;  // fully masked warp
-            double Ss = act ? (double)w_S[l][wi] * f : 0.0;
-            double Ks = 0.0;
-            if (act && l > 0 && f != 0.0)
-                Ks = ((double)w_K[l][wi] + ((double)mw - (double)w_m[l - 1][wi]) * (double)w_S[l][wi]) * f;
-            int am = (act && mw == ms) ? w_am[l][wi] : 0x7fffffff;
+            double Ss = act ? (double)c.rec1[q][l][wi].S : 0.0;
+            double Ks = act ? (double)c.rec1[q][l][wi].K : 0.0;
+            int am = act ? c.rec1[q][l][wi].am : 0x7fffffff;
 #pragma unroll
             for (int o = 4; o > 0; o >>= 1) {
                 Ss += __shfl_xor_sync(0xffffffffu, Ss, o);
@@ -179,105 +387,108 @@ __global__ void __launch_bounds__(T, 2) core_kernel(CoreParams p) {
                 am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
             }
             if (act && wi == 0) {
+                const float m = c.ms[q][l];
                 Partial pr;
-                pr.m = ms;
+                pr.m = m;
                 pr.amax = am;
                 pr.S = Ss;
-                pr.Kl = Ks;
-                p.partials[((size_t)u * L + l) * p.C + s] = pr;
+                // restore the per-slice KL shift (m_l - m_{l-1}) in float64
+                pr.Kl = l > 0 ? Ks + ((double)m - (double)c.ms[q][l > 0 ? l - 1 : 0]) * Ss : 0.0;
+                p.partials[((size_t)u * L + l) * C + s] = pr;
             }
-            __threadfence();
             __syncwarp();
-            if (lane == 0) s_last = (atomicAdd(&p.cnt[u], 1u) == (uint32_t)(p.C - 1));
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (warp < L) {
-                double Kl;
-                RowStat r = combine_row(p.partials + ((size_t)u * L + warp) * p.C, p.C, &Kl);
-                if (lane == 0) {
-                    s_row[warp] = r;
-                    s_K[warp] = Kl;
-                    p.rowstat[(size_t)u * L + warp] = r;
-                }
-            }
-            __syncthreads();
-            if (tid == 0) {
-                bool bad = false;
-#pragma unroll
-                for (int l = 0; l < L; ++l) bad |= s_row[l].bad != 0;
-#pragma unroll
-                for (int l = 1; l < L; ++l) {
-                    double kl = s_K[l] / s_row[l].S - (s_row[l].lse - s_row[l - 1].lse);
-                    p.kl[(size_t)u * (L - 1) + (l - 1)] = kl;
-                }
-                if (bad) atomicOr(&p.flags[b], (uint32_t)MSD_F_NONFINITE);
+            uint32_t old = 0;
+            if (lane == 0) {
                 __threadfence();
-                st_release_u32(&p.ready[u], 1u);
+                old = atom_add_acqrel(&p.cnt[u], 1u);
             }
-        } else {
-            if (tid == 0) {
+            // the previous item's counter result is examined one item late (latency hiding)
+            if (prev_u >= 0 && __shfl_sync(0xffffffffu, prev_old, 0) == (uint32_t)(C - 1)) combine_unit(prev_u);
+            prev_u = u;
+            prev_old = old;
+        }
+        if (prev_u >= 0 && __shfl_sync(0xffffffffu, prev_old, 0) == (uint32_t)(C - 1)) combine_unit(prev_u);
+    } else if (warp == W_FETCH) {
+        // ================================================================ fetcher (pass-2 factors)
+        constexpr int GF = 4;
+        for (int64_t j0 = 0; j0 < n_my; j0 += GF) {
+            const int64_t jj = j0 + lane;
+            RowF f[L];
+            if (lane < GF && jj < n_my) {
+                int64_t u, b, i;
+                int s;
+                item(jj, u, s, b, i);
                 const uint64_t t0 = globaltimer();
                 while (ld_acquire_u32(&p.ready[u]) == 0u) {
-                    __nanosleep(64);
-                    if (globaltimer() - t0 > 4000000000ull) {  // 4 s watchdog
+                    __nanosleep(32);
+                    if (globaltimer() - t0 > 4000000000ull) {
                         atomicOr(p.err, 1u);
                         atomicOr(&p.flags[b], (uint32_t)MSD_F_TIMEOUT);
                         break;
                     }
                 }
-            }
-            __syncthreads();
-            if (tid < L) {
-                const RowStat* g = p.rowstat + (size_t)u * L + tid;
-                RowStat r;
-                r.M = __ldcg(&g->M);
-                r.S = __ldcg(&g->S);
-                r.lse = __ldcg(&g->lse);
-                r.amax = __ldcg(&g->amax);
-                r.bad = __ldcg(&g->bad);
-                s_row[tid] = r;
-            }
-        }
-        __syncthreads();
-
-        // ---------------- pass 2: residual mass of each adjacent pair in this slice
-        double c_self = 0.0;   // lane l: exp(m_w,l - M_l)
-        if (lane < L) {
-            float wml = wm_r[0];
+                double cl[L], Sl[L];
 #pragma unroll
-            for (int l = 1; l < L; ++l)
-                if (lane == l) wml = wm_r[l];
-            c_self = (wml > NEG_MASKED) ? exp((double)wml - s_row[lane].M) : 0.0;
-        }
+                for (int l = 0; l < L; ++l) {
+                    const RowStat* g = p.rowstat + (size_t)u * L + l;
+                    const double M = __ldcg(&g->M);
+                    Sl[l] = __ldcg(&g->S);
+                    const float m = __ldcg(&p.partials[((size_t)u * L + l) * C + s].m);
+                    cl[l] = (m > NEG_MASKED) ? exp((double)m - M) : 0.0;
+                }
+                f[0].rho_hi = f[0].rho_lo = 0.f;
+                f[0].scale = 0.0;
+                f[0].skip = 1;
+                f[0].pad = 0;
 #pragma unroll
-        for (int l = 1; l < L; ++l) {
-            const double ca = __shfl_sync(0xffffffffu, c_self, l);
-            const double cb = __shfl_sync(0xffffffffu, c_self, l - 1);
-            float acc = 0.f;
-            if (ca > 0.0) {
-                const double rho = cb * s_row[l].S / (s_row[l - 1].S * ca);
-                const float rh = (float)rho;
-                const float rl = (float)(rho - (double)rh);
-#pragma unroll
-                for (int k = 0; k < ET; ++k) {
-                    float t = fmaf(-e[l - 1][k], rh, e[l][k]);
-                    t = fmaf(-e[l - 1][k], rl, t);
-                    acc += fmaxf(t, 0.f);
+                for (int l = 1; l < L; ++l) {
+                    const bool skip = !(cl[l] > 0.0) || !(Sl[l] > 0.0) || !(Sl[l - 1] > 0.0);
+                    const double rho = skip ? 0.0 : cl[l - 1] * Sl[l] / (Sl[l - 1] * cl[l]);
+                    f[l].rho_hi = (float)rho;
+                    f[l].rho_lo = (float)(rho - (double)f[l].rho_hi);
+                    f[l].scale = skip ? 0.0 : cl[l] / Sl[l];
+                    f[l].skip = skip ? 1 : 0;
+                    f[l].pad = 0;
                 }
             }
-            acc = warp_sum(acc);
-            if (lane == 0) w_R[l][warp] = (double)acc * ca;
-        }
-        __syncthreads();
-        if (warp == 0 && lane >= 1 && lane < L) {
-            double R = 0.0;
+            for (int g = 0; g < GF && j0 + g < n_my; ++g) {
+                const int64_t jg = j0 + g;
+                const int q = (int)(jg % NR);
+                if (jg >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((jg / NR) - 1) & 1));
+                if (lane == g) {
 #pragma unroll
-            for (int wi = 0; wi < NWARP; ++wi) R += w_R[lane][wi];
-            p.resid[((size_t)u * (L - 1) + (lane - 1)) * p.C + s] = R / s_row[lane].S;
+                    for (int l = 0; l < L; ++l) c.rowf[q][l] = f[l];
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&c.rowf_full[q]);
+            }
+        }
+    } else if (warp == W_RED) {
+        // ================================================================ reducer (slice residual)
+        for (int64_t j = 0; j < n_my; ++j) {
+            int64_t u, b, i;
+            int s;
+            item(j, u, s, b, i);
+            const int q = (int)(j % NR);
+            mbar_wait(&c.rec2_full[q], (uint32_t)((j / NR) & 1));
+            const int l = 1 + (lane >> 3), wi = lane & 7;
+            const bool act = l < L;
+            double R = act ? c.rec2[q][l][wi] : 0.0;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
+            if (act && wi == 0) {
+                const double v = c.rec2_skip[q][l] ? 0.0 : R * c.rec2_scale[q][l];
+                p.resid[((size_t)u * (L - 1) + (l - 1)) * C + s] = v;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c.rec2_empty[q]);
         }
     }
+
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == W_PROD) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(c.taddr));
 }
 
 template <typename Tin, int L, bool G>
@@ -285,25 +496,25 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     CoreParams p = p0;
     const int ES = (int)sizeof(Tin);
     const size_t stage_bytes = (size_t)L * VS * ES;
-    int S = (int)(98304 / stage_bytes);
+    int S = (int)(147456 / stage_bytes);
     if (S < 2) S = 2;
-    if (S > 4) S = 4;
+    if (S > SMAX) S = SMAX;
     p.stages = S;
-    const size_t smem = stage_bytes * S + 64;
+    const size_t smem = align_up(stage_bytes * S, 128) + sizeof(Ctl<L>) + 128;
     auto k = core_kernel<Tin, L, G>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, T, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, CORE_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    int64_t grid = (int64_t)nsm * occ;
+    int64_t grid = nsm;                    // one CTA per SM (it owns all 512 TMEM columns)
     if (grid > p.n_items) grid = p.n_items;
-    if (grid < p.C) return cudaErrorInvalidConfiguration;  // never: C <= 128 < 148
+    if (grid < p.C && grid < p.n_items) return cudaErrorInvalidConfiguration;
     void* args[] = {&p};
-    return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(T), args, smem, s);
+    return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(CORE_THREADS), args, smem, s);
 }
 
 cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s) {
