@@ -135,6 +135,7 @@ msd_status run_engine(const Engine& E) {
     cp.C = w.C; cp.U = w.U;
     cp.n_items = (int64_t)w.U * w.C;
     cp.partials = reinterpret_cast<Partial*>(ws + w.partials);
+    cp.partms = reinterpret_cast<float2*>(ws + w.partms);
     cp.rowstat = reinterpret_cast<RowStat*>(ws + w.rowstat);
     cp.kl = reinterpret_cast<double*>(ws + w.kl);
     cp.resid = reinterpret_cast<double*>(ws + w.resid);

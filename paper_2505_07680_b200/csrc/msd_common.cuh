@@ -45,7 +45,7 @@ struct RowStat {
 
 // Workspace layout (bytes), shared by host and device code.
 struct WsLayout {
-    size_t hdr, cnt, ready, partials, rowstat, kl, resid, total;
+    size_t hdr, cnt, ready, partials, partms, rowstat, kl, resid, total;
     int32_t U, C, L;
 };
 
@@ -62,6 +62,7 @@ __host__ __device__ inline WsLayout ws_layout(int32_t L, int32_t B, int32_t K, i
     w.cnt = off;      off = align_up(off + sizeof(uint32_t) * (size_t)w.U, 256);
     w.ready = off;    off = align_up(off + sizeof(uint32_t) * (size_t)w.U, 256);
     w.partials = off; off = align_up(off + sizeof(Partial) * (size_t)w.U * L * w.C, 256);
+    w.partms = off;   off = align_up(off + sizeof(float2) * (size_t)w.U * L * w.C, 256);
     w.rowstat = off;  off = align_up(off + sizeof(RowStat) * (size_t)w.U * L, 256);
     w.kl = off;       off = align_up(off + sizeof(double) * (size_t)w.U * (L - 1), 256);
     w.resid = off;    off = align_up(off + sizeof(double) * (size_t)w.U * (L - 1) * w.C, 256);

@@ -10,7 +10,7 @@
 // SM): CTA g processes items g, g+G, g+2G, ...; the C items of a unit run
 // concurrently on C CTAs, which exchange per-slice partials through global memory.
 //
-// Warp specialisation (12 warps):
+// Warp specialisation (13 warps):
 //   warps 0-7  compute: pass 1 of item j  -- slice max (named barrier among compute
 //                warps), e_v = 2^((z_v - m_s) log2 e) (one MUFU.EX2 per element), sums S
 //                and the KL numerator, e_v parked in TMEM (tcgen05.st);
@@ -19,11 +19,12 @@
 //   warp 8     producer: TMA bulk copies (cp.async.bulk) of the L row slices into an
 //                S-stage shared-memory ring.
 //   warp 9     publisher: folds the compute warps' records into the slice partial,
-//                publishes it, and -- when it is the unit's last slice -- combines the
-//                C partials (float64, fixed order) into the unit's row statistics.
-//   warp 10    fetcher: waits until an item's unit statistics are released and turns
-//                them into the pass-2 factors of that slice (float64).
-//   warp 11    reducer: sums the pass-2 warp records into the slice residual R_s.
+//                publishes it and bumps the unit counter (release); the CTA completing
+//                a unit later combines its row statistics for the tail kernel (idle time).
+//   warps 10,11 fetchers (even / odd items): wait for the unit counter, combine the
+//                unit's compact partials (float64, fixed order) and derive this slice's
+//                pass-2 factors.
+//   warp 12    reducer: sums the pass-2 warp records into the slice residual R_s.
 // The exchange latency is hidden behind LAG items of pass 1 (TMEM holds LAG+1 items
 // of exponentials per compute thread: 256 columns / (16 L)).
 #include "msd_common.cuh"
@@ -33,8 +34,9 @@ namespace msd {
 
 constexpr int NCW = 8;                 // compute warps
 constexpr int CT = NCW * 32;           // compute threads (the slice mapping uses CT == T)
-constexpr int CORE_THREADS = CT + 4 * 32;
-constexpr int W_PROD = 8, W_PUB = 9, W_FETCH = 10, W_RED = 11;
+constexpr int CORE_THREADS = CT + 5 * 32;
+constexpr int W_PROD = 8, W_PUB = 9, W_FETCH0 = 10, W_FETCH1 = 11, W_RED = 12;
+constexpr int NDEFER = 64;
 constexpr int SMAX = 6;
 constexpr int NRMAX = 8;
 static_assert(CT == T, "slice mapping assumes 256 compute threads");
@@ -62,6 +64,7 @@ struct Ctl {
     double rec2[NRMAX][L][NWARP];
     double rec2_scale[NRMAX][L];
     int rec2_skip[NRMAX][L];
+    int64_t defer[NDEFER];       // units whose tail-side combine this CTA owes (publisher-private)
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -69,11 +72,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t* p, uint32_t v) {
+__device__ __forceinline__ uint32_t atom_add_release(uint32_t* p, uint32_t v) {
     uint32_t r;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
     return r;
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ void tm_st16(uint32_t ta, const float* v) {
     asm volatile(
@@ -344,11 +357,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             }
         }
     } else if (warp == W_PUB) {
-        // ================================================================ publisher / combiner
-        int64_t prev_u = -1;
-        uint32_t prev_old = 0;
+        // ================================================================ publisher
+        // Publishes each item's slice partial (compact (m, S) for the pass-2 exchange, full
+        // record for the tail) and bumps the unit counter with release semantics.  The CTA
+        // that completes a unit owes the unit's row statistics / KL to the tail kernel; that
+        // combine is off the critical path and runs whenever the publisher is idle.
+        int nd = 0, hd = 0;
         auto combine_unit = [&](int64_t u) {
-            __threadfence();
+            fence_acq_rel_gpu();
             RowStat rs[L];
             double Kl[L];
 #pragma unroll
@@ -364,8 +380,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 for (int l = 1; l < L; ++l)
                     p.kl[(size_t)u * (L - 1) + (l - 1)] = Kl[l] / rs[l].S - (rs[l].lse - rs[l - 1].lse);
                 if (bad) atomicOr(&p.flags[u / p.K], (uint32_t)MSD_F_NONFINITE);
-                __threadfence();
-                st_release_u32(&p.ready[u], 1u);
             }
             __syncwarp();
         };
@@ -374,7 +388,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             int s;
             item(j, u, s, b, i);
             const int q = (int)(j % NR);
-            mbar_wait(&c.rec1_full[q], (uint32_t)((j / NR) & 1));
+            const uint32_t par = (uint32_t)((j / NR) & 1);
+            while (!mbar_test(&c.rec1_full[q], par)) {
+                if (hd < nd) combine_unit(c.defer[(hd++) % NDEFER]);
+                else __nanosleep(20);
+            }
             const int l = lane >> 3, wi = lane & 7;
             const bool act = l < L;
             double Ss = act ? (double)c.rec1[q][l][wi].S : 0.0;
@@ -386,82 +404,107 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 Ks += __shfl_xor_sync(0xffffffffu, Ks, o);
                 am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
             }
-            if (act && wi == 0) {
-                const float m = c.ms[q][l];
-                Partial pr;
-                pr.m = m;
-                pr.amax = am;
-                pr.S = Ss;
-                // restore the per-slice KL shift (m_l - m_{l-1}) in float64
-                pr.Kl = l > 0 ? Ks + ((double)m - (double)c.ms[q][l > 0 ? l - 1 : 0]) * Ss : 0.0;
-                p.partials[((size_t)u * L + l) * C + s] = pr;
+            // lane 0 writes every row's records itself so its release covers them
+            double Sr[L], Kr[L];
+            int ar[L];
+#pragma unroll
+            for (int r = 0; r < L; ++r) {
+                Sr[r] = __shfl_sync(0xffffffffu, Ss, r * 8);
+                Kr[r] = __shfl_sync(0xffffffffu, Ks, r * 8);
+                ar[r] = __shfl_sync(0xffffffffu, am, r * 8);
             }
-            __syncwarp();
             uint32_t old = 0;
             if (lane == 0) {
-                __threadfence();
-                old = atom_add_acqrel(&p.cnt[u], 1u);
+#pragma unroll
+                for (int r = 0; r < L; ++r) {
+                    const float m = c.ms[q][r];
+                    const size_t idx = ((size_t)u * L + r) * C + s;
+                    p.partms[idx] = make_float2(m, (float)Sr[r]);
+                    Partial pr;
+                    pr.m = m;
+                    pr.amax = ar[r];
+                    pr.S = Sr[r];
+                    // restore the per-slice KL shift (m_l - m_{l-1}) in float64
+                    pr.Kl = r > 0 ? Kr[r] + ((double)m - (double)c.ms[q][r > 0 ? r - 1 : 0]) * Sr[r] : 0.0;
+                    p.partials[idx] = pr;
+                }
+                old = atom_add_release(&p.cnt[u], 1u);
             }
-            // the previous item's counter result is examined one item late (latency hiding)
-            if (prev_u >= 0 && __shfl_sync(0xffffffffu, prev_old, 0) == (uint32_t)(C - 1)) combine_unit(prev_u);
-            prev_u = u;
-            prev_old = old;
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old == (uint32_t)(C - 1)) {
+                if (nd - hd >= NDEFER) combine_unit(c.defer[(hd++) % NDEFER]);
+                if (lane == 0) c.defer[nd % NDEFER] = u;
+                __syncwarp();
+                ++nd;
+            }
         }
-        if (prev_u >= 0 && __shfl_sync(0xffffffffu, prev_old, 0) == (uint32_t)(C - 1)) combine_unit(prev_u);
-    } else if (warp == W_FETCH) {
-        // ================================================================ fetcher (pass-2 factors)
-        constexpr int GF = 4;
-        for (int64_t j0 = 0; j0 < n_my; j0 += GF) {
-            const int64_t jj = j0 + lane;
-            RowF f[L];
-            if (lane < GF && jj < n_my) {
-                int64_t u, b, i;
-                int s;
-                item(jj, u, s, b, i);
+        while (hd < nd) combine_unit(c.defer[(hd++) % NDEFER]);
+    } else if (warp == W_FETCH0 || warp == W_FETCH1) {
+        // ================================================================ fetchers (pass-2 factors)
+        // Fetcher f serves items j = f (mod 2), in order: wait for the unit counter, read the
+        // unit's compact partials, combine them (float64, fixed order) and derive this slice's
+        // pass-2 factors.  It only ever blocks on the item the compute warps need next.
+        const int f = warp - W_FETCH0;
+        for (int64_t j = f; j < n_my; j += 2) {
+            int64_t u, b, i;
+            int s;
+            item(j, u, s, b, i);
+            const int q = (int)(j % NR);
+            if (lane == 0) {
                 const uint64_t t0 = globaltimer();
-                while (ld_acquire_u32(&p.ready[u]) == 0u) {
-                    __nanosleep(32);
+                while (ld_acquire_u32(&p.cnt[u]) < (uint32_t)C) {
                     if (globaltimer() - t0 > 4000000000ull) {
                         atomicOr(p.err, 1u);
                         atomicOr(&p.flags[b], (uint32_t)MSD_F_TIMEOUT);
                         break;
                     }
                 }
-                double cl[L], Sl[L];
+            }
+            __syncwarp();
+            double Ml[L], Sl[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                const float2* pm = p.partms + ((size_t)u * L + l) * C;
+                float m = -INFINITY;
+                for (int t = lane; t < C; t += 32) m = fmaxf(m, __ldcg(&pm[t]).x);
+                m = warp_max(m);
+                double S = 0.0;
+                for (int t = lane; t < C; t += 32) {
+                    const float2 v = __ldcg(&pm[t]);
+                    S += (double)v.y * exp((double)v.x - (double)m);
+                }
+                Sl[l] = warp_sum_d(S);
+                Ml[l] = (double)m;
+            }
+            RowF fr[L];
+            if (lane == 0) {
+                double cl[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
-                    const RowStat* g = p.rowstat + (size_t)u * L + l;
-                    const double M = __ldcg(&g->M);
-                    Sl[l] = __ldcg(&g->S);
-                    const float m = __ldcg(&p.partials[((size_t)u * L + l) * C + s].m);
-                    cl[l] = (m > NEG_MASKED) ? exp((double)m - M) : 0.0;
+                    const float m = c.ms[q][l];
+                    cl[l] = (m > NEG_MASKED && Ml[l] > NEG_MASKED) ? exp((double)m - Ml[l]) : 0.0;
                 }
-                f[0].rho_hi = f[0].rho_lo = 0.f;
-                f[0].scale = 0.0;
-                f[0].skip = 1;
-                f[0].pad = 0;
+                fr[0].rho_hi = fr[0].rho_lo = 0.f;
+                fr[0].scale = 0.0;
+                fr[0].skip = 1;
+                fr[0].pad = 0;
 #pragma unroll
                 for (int l = 1; l < L; ++l) {
-                    const bool skip = !(cl[l] > 0.0) || !(Sl[l] > 0.0) || !(Sl[l - 1] > 0.0);
+                    const bool skip = !(cl[l] > 0.0) || !(Sl[l] > 0.0) || !(Sl[l - 1] > 0.0) || !isfinite(Sl[l]) ||
+                                      !isfinite(Sl[l - 1]);
                     const double rho = skip ? 0.0 : cl[l - 1] * Sl[l] / (Sl[l - 1] * cl[l]);
-                    f[l].rho_hi = (float)rho;
-                    f[l].rho_lo = (float)(rho - (double)f[l].rho_hi);
-                    f[l].scale = skip ? 0.0 : cl[l] / Sl[l];
-                    f[l].skip = skip ? 1 : 0;
-                    f[l].pad = 0;
+                    fr[l].rho_hi = (float)rho;
+                    fr[l].rho_lo = (float)(rho - (double)fr[l].rho_hi);
+                    fr[l].scale = skip ? 0.0 : cl[l] / Sl[l];
+                    fr[l].skip = skip ? 1 : 0;
+                    fr[l].pad = 0;
                 }
-            }
-            for (int g = 0; g < GF && j0 + g < n_my; ++g) {
-                const int64_t jg = j0 + g;
-                const int q = (int)(jg % NR);
-                if (jg >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((jg / NR) - 1) & 1));
-                if (lane == g) {
+                if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
 #pragma unroll
-                    for (int l = 0; l < L; ++l) c.rowf[q][l] = f[l];
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&c.rowf_full[q]);
+                for (int l = 0; l < L; ++l) c.rowf[q][l] = fr[l];
+                mbar_arrive(&c.rowf_full[q]);
             }
+            __syncwarp();
         }
     } else if (warp == W_RED) {
         // ================================================================ reducer (slice residual)

@@ -26,6 +26,7 @@ struct CoreParams {
     int64_t n_items;
     int32_t stages;
     Partial* partials;
+    float2* partms;     // compact (slice max, slice sum) for the pass-2 exchange
     RowStat* rowstat;
     double* kl;
     double* resid;
