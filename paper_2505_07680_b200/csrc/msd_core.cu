@@ -10,7 +10,7 @@
 // SM): CTA g processes items g, g+G, g+2G, ...; the C items of a unit run
 // concurrently on C CTAs, which exchange per-slice partials through global memory.
 //
-// Warp specialisation (13 warps):
+// Warp specialisation (15 warps):
 //   warps 0-7  compute: pass 1 of item j  -- slice max (named barrier among compute
 //                warps), e_v = 2^((z_v - m_s) log2 e) (one MUFU.EX2 per element), sums S
 //                and the KL numerator, e_v parked in TMEM (tcgen05.st);
@@ -21,10 +21,10 @@
 //   warp 9     publisher: folds the compute warps' records into the slice partial,
 //                publishes it and bumps the unit counter (release); the CTA completing
 //                a unit later combines its row statistics for the tail kernel (idle time).
-//   warps 10,11 fetchers (even / odd items): wait for the unit counter, combine the
+//   warps 10-13 fetchers (items j = f mod 4): wait for the unit counter, combine the
 //                unit's compact partials (float64, fixed order) and derive this slice's
 //                pass-2 factors.
-//   warp 12    reducer: sums the pass-2 warp records into the slice residual R_s.
+//   warp 14    reducer: sums the pass-2 warp records into the slice residual R_s.
 // The exchange latency is hidden behind LAG items of pass 1 (TMEM holds LAG+1 items
 // of exponentials per compute thread: 256 columns / (16 L)).
 #include "msd_common.cuh"
@@ -34,8 +34,9 @@ namespace msd {
 
 constexpr int NCW = 8;                 // compute warps
 constexpr int CT = NCW * 32;           // compute threads (the slice mapping uses CT == T)
-constexpr int CORE_THREADS = CT + 5 * 32;
-constexpr int W_PROD = 8, W_PUB = 9, W_FETCH0 = 10, W_FETCH1 = 11, W_RED = 12;
+constexpr int NFETCH = 4;              // fetcher warps (items j = f mod NFETCH)
+constexpr int CORE_THREADS = CT + (3 + NFETCH) * 32;
+constexpr int W_PROD = 8, W_PUB = 9, W_FETCH0 = 10, W_RED = W_FETCH0 + NFETCH;
 constexpr int NDEFER = 64;
 constexpr int SMAX = 6;
 constexpr int NRMAX = 8;
@@ -87,6 +88,11 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
     return done != 0;
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
 
 __device__ __forceinline__ void tm_st16(uint32_t ta, const float* v) {
     asm volatile(
@@ -439,45 +445,63 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             }
         }
         while (hd < nd) combine_unit(c.defer[(hd++) % NDEFER]);
-    } else if (warp == W_FETCH0 || warp == W_FETCH1) {
+    } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
         // ================================================================ fetchers (pass-2 factors)
-        // Fetcher f serves items j = f (mod 2), in order: wait for the unit counter, read the
-        // unit's compact partials, combine them (float64, fixed order) and derive this slice's
-        // pass-2 factors.  It only ever blocks on the item the compute warps need next.
+        // Fetcher f serves items j = f (mod NFETCH) in order: wait for the unit counter
+        // (relaxed polling, one acquire fence), load the unit's L*C compact partials in one
+        // round trip, combine them (float64, fixed order) and derive this slice's pass-2
+        // factors.  A fetcher only ever blocks on the next item it owns.
+        constexpr int MAXT = (MAXL * 128 + 31) / 32;
         const int f = warp - W_FETCH0;
-        for (int64_t j = f; j < n_my; j += 2) {
+        const int LC = L * C;
+        for (int64_t j = f; j < n_my; j += NFETCH) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
             const int q = (int)(j % NR);
             if (lane == 0) {
                 const uint64_t t0 = globaltimer();
-                while (ld_acquire_u32(&p.cnt[u]) < (uint32_t)C) {
+                while (ld_relaxed_u32(&p.cnt[u]) < (uint32_t)C) {
                     if (globaltimer() - t0 > 4000000000ull) {
                         atomicOr(p.err, 1u);
                         atomicOr(&p.flags[b], (uint32_t)MSD_F_TIMEOUT);
                         break;
                     }
                 }
+                fence_acq_rel_gpu();
             }
             __syncwarp();
+            const float2* pm = p.partms + (size_t)u * LC;
+            float2 v[MAXT];
+#pragma unroll
+            for (int t = 0; t < MAXT; ++t) {
+                const int idx = t * 32 + lane;
+                v[t] = idx < LC ? __ldcg(&pm[idx]) : make_float2(-INFINITY, 0.f);
+            }
             double Ml[L], Sl[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                const float2* pm = p.partms + ((size_t)u * L + l) * C;
                 float m = -INFINITY;
-                for (int t = lane; t < C; t += 32) m = fmaxf(m, __ldcg(&pm[t]).x);
-                m = warp_max(m);
+#pragma unroll
+                for (int t = 0; t < MAXT; ++t) {
+                    const int idx = t * 32 + lane;
+                    if (idx >= l * C && idx < (l + 1) * C) m = fmaxf(m, v[t].x);
+                }
+                Ml[l] = (double)warp_max(m);
+            }
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
                 double S = 0.0;
-                for (int t = lane; t < C; t += 32) {
-                    const float2 v = __ldcg(&pm[t]);
-                    S += (double)v.y * exp((double)v.x - (double)m);
+#pragma unroll
+                for (int t = 0; t < MAXT; ++t) {
+                    const int idx = t * 32 + lane;
+                    if (idx >= l * C && idx < (l + 1) * C && v[t].x > NEG_MASKED)
+                        S += (double)v[t].y * exp((double)v[t].x - Ml[l]);
                 }
                 Sl[l] = warp_sum_d(S);
-                Ml[l] = (double)m;
             }
-            RowF fr[L];
             if (lane == 0) {
+                RowF fr[L];
                 double cl[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
