@@ -25,6 +25,7 @@ constexpr float NEG_CLAMP = -1e30f;  // logits are clamped to >= this (NaN kept)
 constexpr float NEG_MASKED = -1e29f; // clamped logits <= this mean "-inf" (p = 0)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr double KL_INF_THRESH = 1e20;
+constexpr int CNT_STRIDE = 64;      // uint32 elements between unit counters (256 B)
 
 // Per (unit, level, slice) pass-1 record, published for the cross-CTA exchange.
 struct Partial {
@@ -59,7 +60,8 @@ __host__ __device__ inline WsLayout ws_layout(int32_t L, int32_t B, int32_t K, i
     w.C = (int32_t)ceil_div(V, VS);
     size_t off = 0;
     w.hdr = off;      off += 256;
-    w.cnt = off;      off = align_up(off + sizeof(uint32_t) * (size_t)w.U, 256);
+    // one counter per 256-byte block: concurrent units' counters must not share an L2 line
+    w.cnt = off;      off = align_up(off + CNT_STRIDE * sizeof(uint32_t) * (size_t)w.U, 256);
     w.ready = off;    off = align_up(off + sizeof(uint32_t) * (size_t)w.U, 256);
     w.partials = off; off = align_up(off + sizeof(Partial) * (size_t)w.U * L * w.C, 256);
     w.partms = off;   off = align_up(off + sizeof(float2) * (size_t)w.U * L * w.C, 256);

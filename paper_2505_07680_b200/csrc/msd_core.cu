@@ -369,6 +369,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // that completes a unit owes the unit's row statistics / KL to the tail kernel; that
         // combine is off the critical path and runs whenever the publisher is idle.
         int nd = 0, hd = 0;
+        int64_t prev_u = -1;
+        uint32_t prev_old = 0;
         auto combine_unit = [&](int64_t u) {
             fence_acq_rel_gpu();
             RowStat rs[L];
@@ -434,15 +436,23 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     pr.Kl = r > 0 ? Kr[r] + ((double)m - (double)c.ms[q][r > 0 ? r - 1 : 0]) * Sr[r] : 0.0;
                     p.partials[idx] = pr;
                 }
-                old = atom_add_release(&p.cnt[u], 1u);
+                old = atom_add_release(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
             }
-            old = __shfl_sync(0xffffffffu, old, 0);
-            if (old == (uint32_t)(C - 1)) {
+            // the counter result of the previous item is examined now (its latency was hidden)
+            const uint32_t po = __shfl_sync(0xffffffffu, prev_old, 0);
+            if (prev_u >= 0 && po == (uint32_t)(C - 1)) {
                 if (nd - hd >= NDEFER) combine_unit(c.defer[(hd++) % NDEFER]);
-                if (lane == 0) c.defer[nd % NDEFER] = u;
+                if (lane == 0) c.defer[nd % NDEFER] = prev_u;
                 __syncwarp();
                 ++nd;
             }
+            prev_u = u;
+            prev_old = old;
+        }
+        if (prev_u >= 0 && __shfl_sync(0xffffffffu, prev_old, 0) == (uint32_t)(C - 1)) {
+            if (lane == 0) c.defer[nd % NDEFER] = prev_u;
+            __syncwarp();
+            ++nd;
         }
         while (hd < nd) combine_unit(c.defer[(hd++) % NDEFER]);
     } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
@@ -461,7 +471,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int q = (int)(j % NR);
             if (lane == 0) {
                 const uint64_t t0 = globaltimer();
-                while (ld_relaxed_u32(&p.cnt[u]) < (uint32_t)C) {
+                while (ld_relaxed_u32(&p.cnt[(size_t)u * CNT_STRIDE]) < (uint32_t)C) {
+                    __nanosleep(128);
                     if (globaltimer() - t0 > 4000000000ull) {
                         atomicOr(p.err, 1u);
                         atomicOr(&p.flags[b], (uint32_t)MSD_F_TIMEOUT);

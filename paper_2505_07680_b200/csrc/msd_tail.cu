@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         if (sh.flags) atomicOr(&p.flags[b], sh.flags);
     }
     for (int i = tid; i < K; i += T) {
-        p.cnt[(size_t)b * K + i] = 0u;
+        p.cnt[((size_t)b * K + i) * CNT_STRIDE] = 0u;
         p.ready[(size_t)b * K + i] = 0u;
     }
 }
