@@ -58,6 +58,9 @@ double env_double(const char* name, double dflt) {
     return v ? atof(v) : dflt;
 }
 
+unsigned long long* g_trace = nullptr;   // debug trace buffer (msd_debug_set_trace)
+size_t g_trace_items = 0;
+
 // ----------------------------------------------------------------- profiling
 struct Prof {
     std::mutex mu;
@@ -143,6 +146,7 @@ msd_status run_engine(const Engine& E) {
     cp.ready = reinterpret_cast<uint32_t*>(ws + w.ready);
     cp.flags = E.flags;
     cp.err = reinterpret_cast<uint32_t*>(ws + w.hdr);
+    cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
 
     TailParams tp;
     memset(&tp, 0, sizeof(tp));
@@ -313,6 +317,12 @@ msd_status msd_kv_rollback(const msd_paged_kv* kv, int32_t n_models, int32_t B,
         cudaError_t e = launch_rollback(p, reinterpret_cast<cudaStream_t>(stream));
         if (e != cudaSuccess) return cuda_fail(e, "msd_rollback launch");
     }
+    return MSD_OK;
+}
+
+msd_status msd_debug_set_trace(void* dev_buf, size_t bytes) {
+    g_trace = reinterpret_cast<unsigned long long*>(dev_buf);
+    g_trace_items = dev_buf ? bytes / 64 : 0;
     return MSD_OK;
 }
 

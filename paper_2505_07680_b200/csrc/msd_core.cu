@@ -152,6 +152,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
+    auto stamp = [&](int64_t j, int k) {
+        if (p.trace) p.trace[(blockIdx.x + j * G) * 8 + k] = globaltimer();
+    };
     auto item = [&](int64_t j, int64_t& u, int& s, int64_t& b, int64_t& i) {
         const int64_t w = blockIdx.x + j * G;
         u = w / C;
@@ -174,6 +177,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int len = (int)min((int64_t)VS, p.V - base);
                 const int len_bulk = (len * ES) / 16 * 16 / ES;
                 mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
+                if (tid == 0) stamp(j, 1);
                 // ---- raw rows -> registers (clamped), warp max per row
                 uint4 raw[L][NV];
 #pragma unroll
@@ -289,6 +293,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 }
                 tm_wait_st();
                 __syncwarp();
+                if (tid == 0) stamp(j, 2);
                 if (lane == 0) {
                     mbar_arrive(&c.empty[st]);
                     mbar_arrive(&c.rec1_full[q]);
@@ -299,6 +304,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int64_t j2 = j - LAG;
                 const int q2 = (int)(j2 % NR);
                 mbar_wait(&c.rowf_full[q2], (uint32_t)((j2 / NR) & 1));
+                if (tid == 0) stamp(j2, 6);
                 RowF f[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) f[l] = c.rowf[q2][l];
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     }
                 }
                 __syncwarp();
+                if (tid == 0) stamp(j2, 7);
                 if (lane == 0) mbar_arrive(&c.rec2_full[q2]);
             }
         }
@@ -351,6 +358,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 item(j, u, s, b, i);
                 const int64_t len = min((int64_t)VS, p.V - (int64_t)s * VS);
                 const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
+                stamp(j, 0);
                 mbar_arrive_expect_tx(&c.full[st], bytes * L);
                 if (bytes) {
 #pragma unroll
@@ -437,6 +445,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     p.partials[idx] = pr;
                 }
                 old = atom_add_release(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
+                stamp(j, 3);
             }
             // the counter result of the previous item is examined now (its latency was hidden)
             const uint32_t po = __shfl_sync(0xffffffffu, prev_old, 0);
@@ -480,6 +489,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     }
                 }
                 fence_acq_rel_gpu();
+                stamp(j, 4);
             }
             __syncwarp();
             const float2* pm = p.partms + (size_t)u * LC;
@@ -537,6 +547,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
 #pragma unroll
                 for (int l = 0; l < L; ++l) c.rowf[q][l] = fr[l];
+                stamp(j, 5);
                 mbar_arrive(&c.rowf_full[q]);
             }
             __syncwarp();

@@ -34,6 +34,7 @@ struct CoreParams {
     uint32_t* ready;
     uint32_t* flags;
     uint32_t* err;
+    unsigned long long* trace;   // debug: 8 globaltimer stamps per item, or NULL
 };
 
 struct TailParams {
