@@ -159,8 +159,8 @@ msd_status run_engine(const Engine& E) {
     tp.n_acc = E.n_acc; tp.m_cand = E.m_cand; tp.out_tok = E.out_tok; tp.out_ld = E.out_ld;
     tp.out_len = E.out_len; tp.rollback = E.rollback;
     tp.pos_dtv = E.pos_dtv; tp.pos_kl = E.pos_kl; tp.stats = E.stats; tp.flags = E.flags;
-    tp.partials = cp.partials; tp.rowstat = cp.rowstat; tp.kl = cp.kl; tp.resid = cp.resid;
-    tp.cnt = cp.cnt; tp.ready = cp.ready;
+    tp.partials = cp.partials; tp.partms = cp.partms; tp.resid = cp.resid;
+    tp.cnt = cp.cnt;
     tp.z_safe = env_double("MSD_Z_SAFE", 0.05);
     tp.exact_all = (int32_t)env_double("MSD_EXACT_DRAWS", 0.0);
 

@@ -7,119 +7,110 @@
 // Decomposition.  A *unit* is one (request b, draft position i < K) and owns the L
 // rows Z_l[b, i, :].  A unit is cut into C slices of VS = 4096 vocabulary entries;
 // an *item* is (unit, slice).  The kernel is persistent and cooperative (one CTA per
-// SM): CTA g processes items g, g+G, g+2G, ...; the C items of a unit run
-// concurrently on C CTAs, which exchange per-slice partials through global memory.
+// SM): CTA g processes items g, g+G, g+2G, ...; the C items of a unit run on C CTAs,
+// which exchange per-slice (max, sum) records through global memory.
 //
-// Warp specialisation (15 warps):
-//   warps 0-7  compute: pass 1 of item j  -- slice max (named barrier among compute
-//                warps), e_v = 2^((z_v - m_s) log2 e) (one MUFU.EX2 per element), sums S
-//                and the KL numerator, e_v parked in TMEM (tcgen05.st);
-//              then pass 2 of item j-LAG -- e_v back from TMEM (tcgen05.ld), residual
-//                mass of each adjacent pair  sum_v max(p_v - q_v, 0)  in this slice.
-//   warp 8     producer: TMA bulk copies (cp.async.bulk) of the L row slices into an
-//                S-stage shared-memory ring.
-//   warp 9     publisher: folds the compute warps' records into the slice partial,
-//                publishes it and bumps the unit counter (release); the CTA completing
-//                a unit later combines its row statistics for the tail kernel (idle time).
-//   warps 10-13 fetchers (items j = f mod 4): wait for the unit counter, combine the
-//                unit's compact partials (float64, fixed order) and derive this slice's
-//                pass-2 factors.
-//   warp 14    reducer: sums the pass-2 warp records into the slice residual R_s.
-// The exchange latency is hidden behind LAG items of pass 1 (TMEM holds LAG+1 items
-// of exponentials per compute thread: 256 columns / (16 L)).
+// Warp specialisation (16 compute + 7 service warps):
+//   compute  pass 1 of item j: per-warp max of each row (the only cross-lane step),
+//            e_v = 2^((z_v - m_w) log2 e) -- one MUFU.EX2 per element --, per-thread sums
+//            (S, KL numerator) to shared memory, e_v parked in TMEM (tcgen05.st);
+//            then pass 2 of item j-LAG: e_v back from TMEM (tcgen05.ld), per-thread residual
+//            sum_v max(p_v - q_v, 0) of every adjacent pair to shared memory.
+//   producer TMA bulk copies (cp.async.bulk) of the L row slices into an S-stage ring.
+//   publisher folds pass-1 records into the slice record (float64 combine), publishes a
+//            self-validating 64-bit (max, sum) record per row with a relaxed store and bumps
+//            the unit counter with a relaxed red (no fence on the critical path).
+//   fetchers (4, items j = f mod 4) poll the unit counter, load the unit's C records in one
+//            round trip (re-loading if one is not yet visible), combine them (float64) into
+//            the row normalisers and derive the per-warp pass-2 factors of this slice.
+//   reducer  folds pass-2 records into the slice residual R_s (float64).
+// The exchange latency hides behind LAG items of pass 1: TMEM holds LAG+1 items of
+// exponentials per compute thread (128 columns / (8 L)).
 #include "msd_common.cuh"
 #include "msd_internal.h"
 
 namespace msd {
 
-constexpr int NCW = 8;                 // compute warps
-constexpr int CT = NCW * 32;           // compute threads (the slice mapping uses CT == T)
-constexpr int NFETCH = 4;              // fetcher warps (items j = f mod NFETCH)
-constexpr int CORE_THREADS = CT + (3 + NFETCH) * 32;
-constexpr int W_PROD = 8, W_PUB = 9, W_FETCH0 = 10, W_RED = W_FETCH0 + NFETCH;
-constexpr int NDEFER = 64;
+constexpr int NCW = 16;                // compute warps
+constexpr int CTH = NCW * 32;          // compute threads
+constexpr int CET = VS / CTH;          // elements per compute thread per row (8)
+constexpr int NFETCH = 4;
+constexpr int W_PROD = NCW, W_PUB = NCW + 1, W_FETCH0 = NCW + 2, W_RED = W_FETCH0 + NFETCH;
+constexpr int CORE_THREADS = (W_RED + 1) * 32;
 constexpr int SMAX = 6;
 constexpr int NRMAX = 8;
-static_assert(CT == T, "slice mapping assumes 256 compute threads");
+constexpr int R1 = 3, R2 = 3;          // pass-1 / pass-2 record rings
+constexpr int NSUB = 4;                // per-warp records after a 3-step shuffle fold (lanes 0..3)
+static_assert(CET == 8, "one 16-byte bf16 vector per thread and row");
 
-struct Rec1 {
-    float S, K;
-    int am;
-    float pad;
-};
-struct RowF {               // pass-2 factors of one row of the current slice
-    float rho_hi, rho_lo;   // rho = c_b S_a / (S_b c_a) for the pair ending at this row
-    double scale;           // c_a / S_a
-    int skip;               // c_a == 0: the slice carries no mass of this row
-    int pad;
+struct WF {                // pass-2 factors of one (row, warp) of the current slice
+    float rho_hi, rho_lo;  // rho = c_b S_a / (S_b c_a)  (pair ending at this row)
+    double scale;          // c_a / S_a
 };
 template <int L>
 struct Ctl {
     uint64_t full[SMAX], empty[SMAX];
-    uint64_t rec1_full[NRMAX], rowf_full[NRMAX], rowf_empty[NRMAX], rec2_full[NRMAX], rec2_empty[NRMAX];
+    uint64_t r1_full[R1], r1_empty[R1], r2_full[R2], r2_empty[R2];
+    uint64_t rowf_full[NRMAX], rowf_empty[NRMAX];
     uint32_t taddr;
-    float wmax[2][L][NWARP];
-    float ms[NRMAX][L];
-    Rec1 rec1[NRMAX][L][NWARP];
-    RowF rowf[NRMAX][L];
-    double rec2[NRMAX][L][NWARP];
-    double rec2_scale[NRMAX][L];
-    int rec2_skip[NRMAX][L];
-    int64_t defer[NDEFER];       // units whose tail-side combine this CTA owes (publisher-private)
+    float wmx[NRMAX][L][NCW];               // per-warp max of each row, per item slot
+    float r1S[R1][L][NCW][NSUB];            // pass-1 partial sums
+    float r1K[R1][L][NCW][NSUB];            // pass-1 KL numerators (relative to the warp shift)
+    int r1A[R1][L][NCW];                    // greedy: first argmax index per warp
+    WF rowf[NRMAX][L][NCW];
+    float r2R[R2][L][NCW][NSUB];            // pass-2 residual partials
+    double r2scale[R2][L][NCW];
+    unsigned long long fbuf[NFETCH][MAXL * 128];   // fetcher staging of a unit's records
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t atom_add_release(uint32_t* p, uint32_t v) {
-    uint32_t r;
-    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
-    return r;
+__device__ __forceinline__ void red_add_relaxed(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t done;
-    asm volatile(
-        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return done != 0;
-}
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
     uint32_t r;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
     return r;
 }
-
-__device__ __forceinline__ void tm_st16(uint32_t ta, const float* v) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
-        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
-        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
-        : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long r;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+    return r;
 }
-__device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
-          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
-        : "r"(ta)
-        : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void tm_st8(uint32_t ta, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, float* v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(ta)
+                 : "memory");
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
 __device__ __forceinline__ uint32_t clamp_bf16x2(uint32_t w) { return max_nan_bf16x2(w, 0xF149F149u); }
+
+// fold a per-lane value into lanes 0..3 (lane k holds the sum over lanes == k mod 4)
+__device__ __forceinline__ float fold4(float v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    return v;
+}
 
 template <typename Tin, int L, bool GREEDY>
 __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
-    constexpr int NV = ET / VEC;
+    constexpr int NV = CET / VEC;           // 1 (bf16) or 2 (f32) vectors per thread and row
     constexpr int ES = (int)sizeof(Tin);
-    constexpr int NR = 256 / (16 * L);      // TMEM item slots per compute thread
+    constexpr int NR = 128 / (CET * L);     // TMEM item slots per compute thread
     constexpr int LAG = NR - 1;
     static_assert(NR <= NRMAX && NR >= 2, "TMEM slots");
     extern __shared__ __align__(128) unsigned char smem[];
@@ -135,13 +126,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     if (warp == W_PROD) {
         if (lane == 0) {
             for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], NCW); }
-            for (int q = 0; q < NR; ++q) {
-                mbar_init(&c.rec1_full[q], NCW);
-                mbar_init(&c.rowf_full[q], 1);
-                mbar_init(&c.rowf_empty[q], NCW);
-                mbar_init(&c.rec2_full[q], NCW);
-                mbar_init(&c.rec2_empty[q], 1);
-            }
+            for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], NCW); mbar_init(&c.r1_empty[r], 1); }
+            for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], NCW); mbar_init(&c.r2_empty[r], 1); }
+            for (int q = 0; q < NR; ++q) { mbar_init(&c.rowf_full[q], 1); mbar_init(&c.rowf_empty[q], NCW); }
             fence_mbar_init();
         }
         __syncwarp();
@@ -165,7 +152,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 
     if (warp < NCW) {
         // ================================================================ compute warps
-        const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
+        const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
         for (int64_t j = 0; j < n_my + LAG; ++j) {
             if (j < n_my) {
                 int64_t u, b, i;
@@ -173,19 +160,20 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 item(j, u, s, b, i);
                 const int st = (int)(j % S);
                 const int q = (int)(j % NR);
+                const int r1 = (int)(j % R1);
                 const int64_t base = (int64_t)s * VS;
                 const int len = (int)min((int64_t)VS, p.V - base);
                 const int len_bulk = (len * ES) / 16 * 16 / ES;
                 mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
                 if (tid == 0) stamp(j, 1);
-                // ---- raw rows -> registers (clamped), warp max per row
                 uint4 raw[L][NV];
+                float tmax[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
                     const Tin* sl = ring + ((size_t)st * L + l) * VS;
 #pragma unroll
                     for (int jv = 0; jv < NV; ++jv) {
-                        const int e0 = (jv * T + tid) * VEC;
+                        const int e0 = (jv * CTH + tid) * VEC;
                         if (e0 + VEC <= len_bulk) {
                             raw[l][jv] = *reinterpret_cast<const uint4*>(sl + e0);
                         } else {   // ragged end of the row: element-wise from smem / global
@@ -203,24 +191,15 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                             raw[l][jv] = *reinterpret_cast<const uint4*>(xs);
                         }
                     }
-                }
-                float msl[L];
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    float tm = -INFINITY;
+                    float tm;
                     if (ES == 2) {
-                        uint32_t mx = 0xFF80FF80u;  // (-inf, -inf)
-#pragma unroll
-                        for (int jv = 0; jv < NV; ++jv) {
-                            raw[l][jv].x = clamp_bf16x2(raw[l][jv].x);
-                            raw[l][jv].y = clamp_bf16x2(raw[l][jv].y);
-                            raw[l][jv].z = clamp_bf16x2(raw[l][jv].z);
-                            raw[l][jv].w = clamp_bf16x2(raw[l][jv].w);
-                            mx = max_nan_bf16x2(mx, max_nan_bf16x2(max_nan_bf16x2(raw[l][jv].x, raw[l][jv].y),
-                                                                   max_nan_bf16x2(raw[l][jv].z, raw[l][jv].w)));
-                        }
+                        uint4& r = raw[l][0];
+                        r.x = clamp_bf16x2(r.x); r.y = clamp_bf16x2(r.y);
+                        r.z = clamp_bf16x2(r.z); r.w = clamp_bf16x2(r.w);
+                        const uint32_t mx = max_nan_bf16x2(max_nan_bf16x2(r.x, r.y), max_nan_bf16x2(r.z, r.w));
                         tm = fmaxf(bf16lo(mx), bf16hi(mx));
                     } else {
+                        tm = -INFINITY;
 #pragma unroll
                         for (int jv = 0; jv < NV; ++jv) {
                             float xs[4];
@@ -230,120 +209,133 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                             tm = fmaxf(tm, fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])));
                         }
                     }
-                    tm = warp_max(tm);
-                    if (lane == 0) c.wmax[j & 1][l][warp] = tm;
+                    tmax[l] = tm;
                 }
-                bar_compute();
+                // per-warp max of all rows, the shuffle chains interleaved
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) tmax[l] = fmaxf(tmax[l], __shfl_xor_sync(0xffffffffu, tmax[l], o));
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
+                }
+                float Sv[L], Kv[L];
+                int am[L];
+                float xprev[CET];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
-                    float m = lane < NWARP ? c.wmax[j & 1][l][lane] : -INFINITY;
-#pragma unroll
-                    for (int o = 4; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    msl[l] = __shfl_sync(0xffffffffu, m, 0);
-                }
-                if (warp == 0 && lane == 0) {
-#pragma unroll
-                    for (int l = 0; l < L; ++l) c.ms[q][l] = msl[l];
-                }
-                // ---- exponentials relative to the slice max, sums, TMEM park
-                float xprev[ET];
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    float x[ET];
+                    float x[CET];
 #pragma unroll
                     for (int jv = 0; jv < NV; ++jv) {
                         const uint4 r = raw[l][jv];
                         if (ES == 2) {
-                            x[jv * 8 + 0] = bf16lo(r.x); x[jv * 8 + 1] = bf16hi(r.x);
-                            x[jv * 8 + 2] = bf16lo(r.y); x[jv * 8 + 3] = bf16hi(r.y);
-                            x[jv * 8 + 4] = bf16lo(r.z); x[jv * 8 + 5] = bf16hi(r.z);
-                            x[jv * 8 + 6] = bf16lo(r.w); x[jv * 8 + 7] = bf16hi(r.w);
+                            x[0] = bf16lo(r.x); x[1] = bf16hi(r.x); x[2] = bf16lo(r.y); x[3] = bf16hi(r.y);
+                            x[4] = bf16lo(r.z); x[5] = bf16hi(r.z); x[6] = bf16lo(r.w); x[7] = bf16hi(r.w);
                         } else {
-                            x[(jv * 4 + 0) % ET] = __uint_as_float(r.x); x[(jv * 4 + 1) % ET] = __uint_as_float(r.y);
-                            x[(jv * 4 + 2) % ET] = __uint_as_float(r.z); x[(jv * 4 + 3) % ET] = __uint_as_float(r.w);
+                            x[(jv * 4 + 0) % CET] = __uint_as_float(r.x); x[(jv * 4 + 1) % CET] = __uint_as_float(r.y);
+                            x[(jv * 4 + 2) % CET] = __uint_as_float(r.z); x[(jv * 4 + 3) % CET] = __uint_as_float(r.w);
                         }
                     }
-                    const float m = msl[l];
-                    const float shift = l > 0 ? m - msl[l > 0 ? l - 1 : 0] : 0.f;
-                    float e[ET];
+                    const float m = tmax[l];
+                    const float shift = l > 0 ? m - tmax[l > 0 ? l - 1 : 0] : 0.f;
+                    float e[CET];
                     float sum = 0.f, ks = 0.f;
 #pragma unroll
-                    for (int k = 0; k < ET; ++k) {
+                    for (int k = 0; k < CET; ++k) {
                         e[k] = ex2f((x[k] - m) * LOG2E);
                         sum += e[k];
                         if (l > 0) ks = fmaf(e[k], (x[k] - xprev[k]) - shift, ks);
                     }
-                    tm_st16(tbase + (uint32_t)(q * 16 * L + l * 16), e);
-                    sum = warp_sum(sum);
-                    if (l > 0) ks = warp_sum(ks);
-                    int am = 0x7fffffff;
+                    tm_st8(tbase + (uint32_t)(q * CET * L + l * CET), e);
+                    Sv[l] = sum;
+                    Kv[l] = ks;
+                    am[l] = 0x7fffffff;
                     if (GREEDY) {
 #pragma unroll
-                        for (int k = ET - 1; k >= 0; --k)
-                            if (x[k] == m) am = (int)(base + ((k / VEC) * T + tid) * VEC + (k % VEC));
-                        am = warp_min_i(am);
-                    }
-                    if (lane == 0) {
-                        Rec1 r;
-                        r.S = sum; r.K = ks; r.am = am; r.pad = 0.f;
-                        c.rec1[q][l][warp] = r;
+                        for (int k = CET - 1; k >= 0; --k)
+                            if (x[k] == m) am[l] = (int)(base + ((k / VEC) * CTH + tid) * VEC + (k % VEC));
                     }
 #pragma unroll
-                    for (int k = 0; k < ET; ++k) xprev[k] = x[k];
+                    for (int k = 0; k < CET; ++k) xprev[k] = x[k];
+                }
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    Sv[l] = fold4(Sv[l]);
+                    if (l > 0) Kv[l] = fold4(Kv[l]);
+                }
+                if (GREEDY) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) am[l] = warp_min_i(am[l]);
+                }
+                if (j >= R1) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
+                if (lane < NSUB) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        c.r1S[r1][l][warp][lane] = Sv[l];
+                        c.r1K[r1][l][warp][lane] = Kv[l];
+                    }
+                    if (GREEDY && lane == 0) {
+#pragma unroll
+                        for (int l = 0; l < L; ++l) c.r1A[r1][l][warp] = am[l];
+                    }
                 }
                 tm_wait_st();
                 __syncwarp();
                 if (tid == 0) stamp(j, 2);
                 if (lane == 0) {
                     mbar_arrive(&c.empty[st]);
-                    mbar_arrive(&c.rec1_full[q]);
+                    mbar_arrive(&c.r1_full[r1]);
                 }
             }
             if (j >= LAG) {
                 // ---- pass 2 of item j2 = j - LAG
                 const int64_t j2 = j - LAG;
                 const int q2 = (int)(j2 % NR);
+                const int r2 = (int)(j2 % R2);
                 mbar_wait(&c.rowf_full[q2], (uint32_t)((j2 / NR) & 1));
                 if (tid == 0) stamp(j2, 6);
-                RowF f[L];
+                float rh[L], rl[L];
+                double sc[L];
 #pragma unroll
-                for (int l = 0; l < L; ++l) f[l] = c.rowf[q2][l];
+                for (int l = 1; l < L; ++l) {
+                    rh[l] = c.rowf[q2][l][warp].rho_hi;
+                    rl[l] = c.rowf[q2][l][warp].rho_lo;
+                    sc[l] = c.rowf[q2][l][warp].scale;
+                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&c.rowf_empty[q2]);
-                float ev[L][ET];
+                float ev[L][CET];
 #pragma unroll
-                for (int l = 0; l < L; ++l) tm_ld16(tbase + (uint32_t)(q2 * 16 * L + l * 16), ev[l]);
+                for (int l = 0; l < L; ++l) tm_ld8(tbase + (uint32_t)(q2 * CET * L + l * CET), ev[l]);
                 tm_wait_ld();
                 float acc[L];
 #pragma unroll
                 for (int l = 1; l < L; ++l) {
                     float a = 0.f;
-                    if (!f[l].skip) {
-                        const float rh = f[l].rho_hi, rl = f[l].rho_lo;
 #pragma unroll
-                        for (int k = 0; k < ET; ++k) {
-                            float t = fmaf(-ev[l - 1][k], rh, ev[l][k]);
-                            t = fmaf(-ev[l - 1][k], rl, t);
-                            a += fmaxf(t, 0.f);
-                        }
+                    for (int k = 0; k < CET; ++k) {
+                        float t = fmaf(-ev[l - 1][k], rh[l], ev[l][k]);
+                        t = fmaf(-ev[l - 1][k], rl[l], t);
+                        a += fmaxf(t, 0.f);
                     }
-                    acc[l] = warp_sum(a);
+                    acc[l] = a;
                 }
-                if (j2 >= NR) mbar_wait(&c.rec2_empty[q2], (uint32_t)(((j2 / NR) - 1) & 1));
+#pragma unroll
+                for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
+                if (j2 >= R2) mbar_wait(&c.r2_empty[r2], (uint32_t)(((j2 / R2) - 1) & 1));
+                if (lane < NSUB) {
+#pragma unroll
+                    for (int l = 1; l < L; ++l) c.r2R[r2][l][warp][lane] = acc[l];
+                }
                 if (lane == 0) {
 #pragma unroll
-                    for (int l = 1; l < L; ++l) c.rec2[q2][l][warp] = (double)acc[l];
-                    if (warp == 0) {
-#pragma unroll
-                        for (int l = 1; l < L; ++l) {
-                            c.rec2_scale[q2][l] = f[l].scale;
-                            c.rec2_skip[q2][l] = f[l].skip;
-                        }
-                    }
+                    for (int l = 1; l < L; ++l) c.r2scale[r2][l][warp] = sc[l];
                 }
                 __syncwarp();
                 if (tid == 0) stamp(j2, 7);
-                if (lane == 0) mbar_arrive(&c.rec2_full[q2]);
+                if (lane == 0) mbar_arrive(&c.r2_full[r2]);
             }
         }
     } else if (warp == W_PROD) {
@@ -372,205 +364,184 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
     } else if (warp == W_PUB) {
         // ================================================================ publisher
-        // Publishes each item's slice partial (compact (m, S) for the pass-2 exchange, full
-        // record for the tail) and bumps the unit counter with release semantics.  The CTA
-        // that completes a unit owes the unit's row statistics / KL to the tail kernel; that
-        // combine is off the critical path and runs whenever the publisher is idle.
-        int nd = 0, hd = 0;
-        int64_t prev_u = -1;
-        uint32_t prev_old = 0;
-        auto combine_unit = [&](int64_t u) {
-            fence_acq_rel_gpu();
-            RowStat rs[L];
-            double Kl[L];
-#pragma unroll
-            for (int l = 0; l < L; ++l) rs[l] = combine_row(p.partials + ((size_t)u * L + l) * C, C, &Kl[l]);
-            if (lane == 0) {
-                bool bad = false;
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    p.rowstat[(size_t)u * L + l] = rs[l];
-                    bad |= rs[l].bad != 0;
-                }
-#pragma unroll
-                for (int l = 1; l < L; ++l)
-                    p.kl[(size_t)u * (L - 1) + (l - 1)] = Kl[l] / rs[l].S - (rs[l].lse - rs[l - 1].lse);
-                if (bad) atomicOr(&p.flags[u / p.K], (uint32_t)MSD_F_NONFINITE);
-            }
-            __syncwarp();
-        };
+        // lane = 2 * w + h: warp w, half h of its NSUB records
+        const int w = lane >> 1, h = lane & 1;
         for (int64_t j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
             const int q = (int)(j % NR);
-            const uint32_t par = (uint32_t)((j / NR) & 1);
-            while (!mbar_test(&c.rec1_full[q], par)) {
-                if (hd < nd) combine_unit(c.defer[(hd++) % NDEFER]);
-                else __nanosleep(20);
-            }
-            const int l = lane >> 3, wi = lane & 7;
-            const bool act = l < L;
-            double Ss = act ? (double)c.rec1[q][l][wi].S : 0.0;
-            double Ks = act ? (double)c.rec1[q][l][wi].K : 0.0;
-            int am = act ? c.rec1[q][l][wi].am : 0x7fffffff;
+            const int r1 = (int)(j % R1);
+            mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
+            float Sw[L], Kw[L], wm[L];
+            int aw[L];
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) {
-                Ss += __shfl_xor_sync(0xffffffffu, Ss, o);
-                Ks += __shfl_xor_sync(0xffffffffu, Ks, o);
-                am = min(am, __shfl_xor_sync(0xffffffffu, am, o));
-            }
-            // lane 0 writes every row's records itself so its release covers them
-            double Sr[L], Kr[L];
-            int ar[L];
+            for (int l = 0; l < L; ++l) {
+                float a = 0.f, k = 0.f;
 #pragma unroll
-            for (int r = 0; r < L; ++r) {
-                Sr[r] = __shfl_sync(0xffffffffu, Ss, r * 8);
-                Kr[r] = __shfl_sync(0xffffffffu, Ks, r * 8);
-                ar[r] = __shfl_sync(0xffffffffu, am, r * 8);
-            }
-            uint32_t old = 0;
-            if (lane == 0) {
-#pragma unroll
-                for (int r = 0; r < L; ++r) {
-                    const float m = c.ms[q][r];
-                    const size_t idx = ((size_t)u * L + r) * C + s;
-                    p.partms[idx] = make_float2(m, (float)Sr[r]);
-                    Partial pr;
-                    pr.m = m;
-                    pr.amax = ar[r];
-                    pr.S = Sr[r];
-                    // restore the per-slice KL shift (m_l - m_{l-1}) in float64
-                    pr.Kl = r > 0 ? Kr[r] + ((double)m - (double)c.ms[q][r > 0 ? r - 1 : 0]) * Sr[r] : 0.0;
-                    p.partials[idx] = pr;
+                for (int t = 0; t < NSUB / 2; ++t) {
+                    a += c.r1S[r1][l][w][h * (NSUB / 2) + t];
+                    k += c.r1K[r1][l][w][h * (NSUB / 2) + t];
                 }
-                old = atom_add_release(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
+                Sw[l] = a + __shfl_xor_sync(0xffffffffu, a, 1);
+                Kw[l] = k + __shfl_xor_sync(0xffffffffu, k, 1);
+                wm[l] = c.wmx[q][l][w];
+                aw[l] = GREEDY ? c.r1A[r1][l][w] : 0x7fffffff;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
+            unsigned long long rec[L];
+            Partial pr[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                float ms = wm[l];
+#pragma unroll
+                for (int o = 16; o > 1; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+                double f = exp((double)wm[l] - (double)ms);
+                if (!(wm[l] > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;   // fully masked warp
+                double Sd = h == 0 ? (double)Sw[l] * f : 0.0;
+                double Kd = 0.0;
+                if (h == 0 && l > 0 && f != 0.0)   // restore the per-warp KL shift in float64
+                    Kd = ((double)Kw[l] + ((double)wm[l] - (double)wm[l > 0 ? l - 1 : 0]) * (double)Sw[l]) * f;
+                int a = (h == 0 && wm[l] == ms) ? aw[l] : 0x7fffffff;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    Sd += __shfl_xor_sync(0xffffffffu, Sd, o);
+                    Kd += __shfl_xor_sync(0xffffffffu, Kd, o);
+                    a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+                }
+                const float Sf = (float)Sd;
+                rec[l] = ((unsigned long long)__float_as_uint(Sf) << 32) | __float_as_uint(ms);
+                pr[l].m = ms;
+                pr[l].amax = a;
+                pr[l].S = Sd;
+                pr[l].Kl = Kd;
+            }
+            if (lane < L) {
+                const size_t idx = ((size_t)u * L + lane) * C + s;
+                unsigned long long rv = rec[0];
+                Partial pv = pr[0];
+#pragma unroll
+                for (int l = 1; l < L; ++l)
+                    if (lane == l) { rv = rec[l]; pv = pr[l]; }
+                p.partials[idx] = pv;
+                st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx, rv);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                red_add_relaxed(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
                 stamp(j, 3);
             }
-            // the counter result of the previous item is examined now (its latency was hidden)
-            const uint32_t po = __shfl_sync(0xffffffffu, prev_old, 0);
-            if (prev_u >= 0 && po == (uint32_t)(C - 1)) {
-                if (nd - hd >= NDEFER) combine_unit(c.defer[(hd++) % NDEFER]);
-                if (lane == 0) c.defer[nd % NDEFER] = prev_u;
-                __syncwarp();
-                ++nd;
-            }
-            prev_u = u;
-            prev_old = old;
         }
-        if (prev_u >= 0 && __shfl_sync(0xffffffffu, prev_old, 0) == (uint32_t)(C - 1)) {
-            if (lane == 0) c.defer[nd % NDEFER] = prev_u;
-            __syncwarp();
-            ++nd;
-        }
-        while (hd < nd) combine_unit(c.defer[(hd++) % NDEFER]);
     } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
         // ================================================================ fetchers (pass-2 factors)
-        // Fetcher f serves items j = f (mod NFETCH) in order: wait for the unit counter
-        // (relaxed polling, one acquire fence), load the unit's L*C compact partials in one
-        // round trip, combine them (float64, fixed order) and derive this slice's pass-2
-        // factors.  A fetcher only ever blocks on the next item it owns.
-        constexpr int MAXT = (MAXL * 128 + 31) / 32;
         const int f = warp - W_FETCH0;
         const int LC = L * C;
+        unsigned long long* fb = c.fbuf[f];
         for (int64_t j = f; j < n_my; j += NFETCH) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
             const int q = (int)(j % NR);
+            const uint64_t t0 = globaltimer();
             if (lane == 0) {
-                const uint64_t t0 = globaltimer();
                 while (ld_relaxed_u32(&p.cnt[(size_t)u * CNT_STRIDE]) < (uint32_t)C) {
-                    __nanosleep(128);
-                    if (globaltimer() - t0 > 4000000000ull) {
-                        atomicOr(p.err, 1u);
-                        atomicOr(&p.flags[b], (uint32_t)MSD_F_TIMEOUT);
-                        break;
-                    }
+                    __nanosleep(100);
+                    if (globaltimer() - t0 > 4000000000ull) break;
                 }
-                fence_acq_rel_gpu();
-                stamp(j, 4);
             }
             __syncwarp();
-            const float2* pm = p.partms + (size_t)u * LC;
-            float2 v[MAXT];
-#pragma unroll
-            for (int t = 0; t < MAXT; ++t) {
-                const int idx = t * 32 + lane;
-                v[t] = idx < LC ? __ldcg(&pm[idx]) : make_float2(-INFINITY, 0.f);
+            if (lane == 0) stamp(j, 4);
+            // stage the unit's records; a record whose sum is still 0 is not yet visible
+            const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
+            while (true) {
+                bool ok = true;
+                for (int idx = lane; idx < LC; idx += 32) {
+                    const unsigned long long r = ld_relaxed_u64(pm + idx);
+                    fb[idx] = r;
+                    ok &= (uint32_t)(r >> 32) != 0u;
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+                if (globaltimer() - t0 > 4000000000ull) {
+                    if (lane == 0) {
+                        atomicOr(p.err, 1u);
+                        atomicOr(&p.flags[b], (uint32_t)MSD_F_TIMEOUT);
+                    }
+                    break;
+                }
+                __nanosleep(64);
             }
+            __syncwarp();
             double Ml[L], Sl[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
                 float m = -INFINITY;
-#pragma unroll
-                for (int t = 0; t < MAXT; ++t) {
-                    const int idx = t * 32 + lane;
-                    if (idx >= l * C && idx < (l + 1) * C) m = fmaxf(m, v[t].x);
-                }
+                for (int t = lane; t < C; t += 32) m = fmaxf(m, __uint_as_float((uint32_t)fb[l * C + t]));
                 Ml[l] = (double)warp_max(m);
+                double Sx = 0.0;
+                for (int t = lane; t < C; t += 32) {
+                    const unsigned long long r = fb[l * C + t];
+                    const float vm = __uint_as_float((uint32_t)r);
+                    if (vm > NEG_MASKED) Sx += (double)__uint_as_float((uint32_t)(r >> 32)) * exp((double)vm - Ml[l]);
+                }
+                Sl[l] = warp_sum_d(Sx);
             }
+            // per-warp factors: lane handles compute warp (lane & 15) for rows of parity (lane >> 4)
+            if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
+            const int w = lane & 15;
+            double cl[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                double S = 0.0;
-#pragma unroll
-                for (int t = 0; t < MAXT; ++t) {
-                    const int idx = t * 32 + lane;
-                    if (idx >= l * C && idx < (l + 1) * C && v[t].x > NEG_MASKED)
-                        S += (double)v[t].y * exp((double)v[t].x - Ml[l]);
-                }
-                Sl[l] = warp_sum_d(S);
+                const float wm = c.wmx[q][l][w];
+                cl[l] = (wm > NEG_MASKED && Ml[l] > NEG_MASKED) ? exp((double)wm - Ml[l]) : 0.0;
             }
+#pragma unroll
+            for (int l = 1; l < L; ++l) {
+                if ((l & 1) != (lane >> 4)) continue;
+                const bool skip = !(cl[l] > 0.0) || !(Sl[l] > 0.0) || !(Sl[l - 1] > 0.0) || !isfinite(Sl[l]) ||
+                                  !isfinite(Sl[l - 1]);
+                const double rho = skip ? 0.0 : cl[l - 1] * Sl[l] / (Sl[l - 1] * cl[l]);
+                WF wf;
+                wf.rho_hi = skip ? 0.f : (float)rho;
+                wf.rho_lo = skip ? 0.f : (float)(rho - (double)wf.rho_hi);
+                wf.scale = skip ? 0.0 : cl[l] / Sl[l];
+                c.rowf[q][l][w] = wf;
+            }
+            __syncwarp();
             if (lane == 0) {
-                RowF fr[L];
-                double cl[L];
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    const float m = c.ms[q][l];
-                    cl[l] = (m > NEG_MASKED && Ml[l] > NEG_MASKED) ? exp((double)m - Ml[l]) : 0.0;
-                }
-                fr[0].rho_hi = fr[0].rho_lo = 0.f;
-                fr[0].scale = 0.0;
-                fr[0].skip = 1;
-                fr[0].pad = 0;
-#pragma unroll
-                for (int l = 1; l < L; ++l) {
-                    const bool skip = !(cl[l] > 0.0) || !(Sl[l] > 0.0) || !(Sl[l - 1] > 0.0) || !isfinite(Sl[l]) ||
-                                      !isfinite(Sl[l - 1]);
-                    const double rho = skip ? 0.0 : cl[l - 1] * Sl[l] / (Sl[l - 1] * cl[l]);
-                    fr[l].rho_hi = (float)rho;
-                    fr[l].rho_lo = (float)(rho - (double)fr[l].rho_hi);
-                    fr[l].scale = skip ? 0.0 : cl[l] / Sl[l];
-                    fr[l].skip = skip ? 1 : 0;
-                    fr[l].pad = 0;
-                }
-                if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
-#pragma unroll
-                for (int l = 0; l < L; ++l) c.rowf[q][l] = fr[l];
                 stamp(j, 5);
                 mbar_arrive(&c.rowf_full[q]);
             }
-            __syncwarp();
         }
     } else if (warp == W_RED) {
         // ================================================================ reducer (slice residual)
+        const int w = lane >> 1, h = lane & 1;
         for (int64_t j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
-            const int q = (int)(j % NR);
-            mbar_wait(&c.rec2_full[q], (uint32_t)((j / NR) & 1));
-            const int l = 1 + (lane >> 3), wi = lane & 7;
-            const bool act = l < L;
-            double R = act ? c.rec2[q][l][wi] : 0.0;
+            const int r2 = (int)(j % R2);
+            mbar_wait(&c.r2_full[r2], (uint32_t)((j / R2) & 1));
+            double R[L];
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) R += __shfl_xor_sync(0xffffffffu, R, o);
-            if (act && wi == 0) {
-                const double v = c.rec2_skip[q][l] ? 0.0 : R * c.rec2_scale[q][l];
-                p.resid[((size_t)u * (L - 1) + (l - 1)) * C + s] = v;
+            for (int l = 1; l < L; ++l) {
+                float a = 0.f;
+#pragma unroll
+                for (int t = 0; t < NSUB / 2; ++t) a += c.r2R[r2][l][w][h * (NSUB / 2) + t];
+                double d = (double)a * c.r2scale[r2][l][w];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                R[l] = d;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&c.rec2_empty[q]);
+            if (lane == 0) mbar_arrive(&c.r2_empty[r2]);
+            if (lane >= 1 && lane < L) {
+                double v = R[1];
+#pragma unroll
+                for (int l = 2; l < L; ++l)
+                    if (lane == l) v = R[l];
+                p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = v;
+            }
         }
     }
 

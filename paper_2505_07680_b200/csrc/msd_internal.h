@@ -58,11 +58,9 @@ struct TailParams {
     msd_pair_stats* stats;
     uint32_t* flags;
     const Partial* partials;
-    const RowStat* rowstat;
-    const double* kl;
+    float2* partms;
     const double* resid;
     uint32_t* cnt;
-    uint32_t* ready;
     double z_safe;
     int32_t exact_all;
 };

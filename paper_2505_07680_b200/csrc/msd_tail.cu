@@ -23,6 +23,8 @@ constexpr int MAXSLICES = 128;   // V <= 524288
 constexpr double TIE_EPS = 1e-6;
 
 struct TailShared {
+    RowStat row[MAXC][MAXL];      // row statistics of draft positions i < K (from the core partials)
+    double kl[MAXC][MAXL];        // KL(p_l || p_{l-1}) at draft position i, l >= 1
     int32_t c[MAXL + 1][MAXC];    // c_l: candidates fed to verifier l (l = 1..L-1); c_L = commit
     int32_t m[MAXL + 1];
     int32_t n[MAXL];
@@ -377,6 +379,23 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         sh.m[1] = m1;
     }
     for (int q = tid; q < MAXL * MAXL; q += T) (&sh.extra_ok[0][0])[q] = 0;
+    // row normalisers (Eq. 1) and KL numerators of every draft-position row, combined from
+    // the core's slice partials in a fixed order (one warp per row)
+    for (int r = warp; r < K * L; r += NWARP) {
+        const int i = r / L, l = r % L;
+        double Kl;
+        RowStat rs = combine_row(p.partials + (((size_t)b * K + i) * L + l) * C, C, &Kl);
+        if (lane == 0) { sh.row[i][l] = rs; sh.kl[i][l] = Kl; }
+    }
+    __syncthreads();
+    if (tid < K) {
+        const int i = tid;
+        bool bad = false;
+        for (int l = 0; l < L; ++l) bad |= sh.row[i][l].bad != 0;
+        for (int l = L - 1; l >= 1; --l)
+            sh.kl[i][l] = sh.kl[i][l] / sh.row[i][l].S - (sh.row[i][l].lse - sh.row[i][l - 1].lse);
+        if (bad) atomicOr(&sh.flags, (uint32_t)MSD_F_NONFINITE);
+    }
     __syncthreads();
     for (int i = tid; i < K; i += T) sh.c[1][i] = p.cand0[b * K + i];
     __syncthreads();
@@ -402,8 +421,8 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
             bool acc = true, tie = false;
             const int i = lane;
             if (i < m) {
-                const RowStat A = i < K ? p.rowstat[((size_t)b * K + i) * L + l] : sh.extra[l][i - K];
-                const RowStat Bq = i < K ? p.rowstat[((size_t)b * K + i) * L + l - 1] : sh.extra[l - 1][i - K];
+                const RowStat A = i < K ? sh.row[i][l] : sh.extra[l][i - K];
+                const RowStat Bq = i < K ? sh.row[i][l - 1] : sh.extra[l - 1][i - K];
                 const int32_t t = sh.c[l][i];
                 if (A.bad || Bq.bad) atomicOr(&sh.flags, (uint32_t)MSD_F_NONFINITE);
                 if (t < 0 || t >= V) {
@@ -445,7 +464,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
             double d = 0.0;
             const double* R = p.resid + (u * (L - 1) + (l - 1)) * C;
             for (int s = 0; s < C; ++s) d += R[s];
-            double kl = p.kl[u * (L - 1) + (l - 1)];
+            double kl = sh.kl[i][l];
             const bool kinf = !(kl < KL_INF_THRESH);
             if (kinf) kl = INFINITY;
             if (p.pos_dtv) p.pos_dtv[((size_t)(l - 1) * p.B + b) * K + i] = (float)d;
@@ -474,8 +493,8 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
             // stats of the rows at `pos`
             RowStat A, Bq;
             if (pos < K) {
-                A = p.rowstat[((size_t)b * K + pos) * L + l];
-                Bq = p.rowstat[((size_t)b * K + pos) * L + l - 1];
+                A = sh.row[pos][l];
+                Bq = sh.row[pos][l - 1];
             } else {
                 if (!resid) {  // bonus row: (re)compute so sh.part holds its slice partials
                     RowStat r = row_stats<Tin>(ra, V, C, sh);
@@ -566,10 +585,10 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         }
         if (sh.flags) atomicOr(&p.flags[b], sh.flags);
     }
-    for (int i = tid; i < K; i += T) {
-        p.cnt[((size_t)b * K + i) * CNT_STRIDE] = 0u;
-        p.ready[(size_t)b * K + i] = 0u;
-    }
+    // reset the core's exchange state of this request's units for the next call
+    for (int i = tid; i < K; i += T) p.cnt[((size_t)b * K + i) * CNT_STRIDE] = 0u;
+    unsigned long long* pm = reinterpret_cast<unsigned long long*>(p.partms) + (size_t)b * K * L * C;
+    for (int t = tid; t < K * L * C; t += T) pm[t] = 0ull;
 }
 
 cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s) {
