@@ -31,17 +31,18 @@
 
 namespace msd {
 
-constexpr int NCW = 16;                // compute warps
-constexpr int CTH = NCW * 32;          // compute threads
-constexpr int CET = VS / CTH;          // elements per compute thread per row (8)
-constexpr int NFETCH = 4;
-constexpr int W_PROD = NCW, W_PUB = NCW + 1, W_FETCH0 = NCW + 2, W_RED = W_FETCH0 + NFETCH;
+constexpr int NCW = 8;                 // pass-1 warps (pass-2 warps: NCW .. 2 NCW - 1)
+constexpr int CTH = NCW * 32;          // pass-1 threads
+constexpr int CET = VS / CTH;          // elements per pass-1 thread per row (16)
+constexpr int NFETCH = 3;
+constexpr int W_P2 = NCW, W_PROD = 2 * NCW, W_PUB = 2 * NCW + 1, W_FETCH0 = 2 * NCW + 2,
+              W_RED = W_FETCH0 + NFETCH;
 constexpr int CORE_THREADS = (W_RED + 1) * 32;
 constexpr int SMAX = 6;
 constexpr int NRMAX = 8;
 constexpr int R1 = 3, R2 = 3;          // pass-1 / pass-2 record rings
 constexpr int NSUB = 4;                // per-warp records after a 3-step shuffle fold (lanes 0..3)
-static_assert(CET == 8, "one 16-byte bf16 vector per thread and row");
+static_assert(CET == 16, "two 16-byte bf16 vectors per thread and row");
 
 struct WF {                // pass-2 factors of one (row, warp) of the current slice
     float rho_hi, rho_lo;  // rho = c_b S_a / (S_b c_a)  (pair ending at this row)
@@ -52,6 +53,7 @@ struct Ctl {
     uint64_t full[SMAX], empty[SMAX];
     uint64_t r1_full[R1], r1_empty[R1], r2_full[R2], r2_empty[R2];
     uint64_t rowf_full[NRMAX], rowf_empty[NRMAX];
+    uint64_t tm_full[NRMAX], tm_empty[NRMAX];   // TMEM item slots: pass-1 warps -> pass-2 warps
     uint32_t taddr;
     float wmx[NRMAX][L][NCW];               // per-warp max of each row, per item slot
     float r1S[R1][L][NCW][NSUB];            // pass-1 partial sums
@@ -82,6 +84,21 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void tm_st16(uint32_t ta, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+          "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+        : "r"(ta)
+        : "memory");
+}
 __device__ __forceinline__ void tm_st8(uint32_t ta, const float* v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
                  "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
@@ -110,8 +127,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NV = CET / VEC;           // 1 (bf16) or 2 (f32) vectors per thread and row
     constexpr int ES = (int)sizeof(Tin);
-    constexpr int NR = 128 / (CET * L);     // TMEM item slots per compute thread
-    constexpr int LAG = NR - 1;
+    constexpr int NR = 256 / (CET * L);     // TMEM item slots (256 columns per pass-1 warp)
     static_assert(NR <= NRMAX && NR >= 2, "TMEM slots");
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = p.stages;
@@ -128,7 +144,12 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], NCW); }
             for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], NCW); mbar_init(&c.r1_empty[r], 1); }
             for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], NCW); mbar_init(&c.r2_empty[r], 1); }
-            for (int q = 0; q < NR; ++q) { mbar_init(&c.rowf_full[q], 1); mbar_init(&c.rowf_empty[q], NCW); }
+            for (int q = 0; q < NR; ++q) {
+                mbar_init(&c.rowf_full[q], 1);
+                mbar_init(&c.rowf_empty[q], NCW);
+                mbar_init(&c.tm_full[q], NCW);
+                mbar_init(&c.tm_empty[q], NCW);
+            }
             fence_mbar_init();
         }
         __syncwarp();
@@ -151,192 +172,209 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     };
 
     if (warp < NCW) {
-        // ================================================================ compute warps
-        const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 128);
-        for (int64_t j = 0; j < n_my + LAG; ++j) {
-            if (j < n_my) {
-                int64_t u, b, i;
-                int s;
-                item(j, u, s, b, i);
-                const int st = (int)(j % S);
-                const int q = (int)(j % NR);
-                const int r1 = (int)(j % R1);
-                const int64_t base = (int64_t)s * VS;
-                const int len = (int)min((int64_t)VS, p.V - base);
-                const int len_bulk = (len * ES) / 16 * 16 / ES;
-                mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
-                if (tid == 0) stamp(j, 1);
-                uint4 raw[L][NV];
-                float tmax[L];
+        // ================================================================ pass-1 warps
+        const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
+        for (int64_t j = 0; j < n_my; ++j) {
+            int64_t u, b, i;
+            int s;
+            item(j, u, s, b, i);
+            const int st = (int)(j % S);
+            const int q = (int)(j % NR);
+            const int r1 = (int)(j % R1);
+            const int64_t base = (int64_t)s * VS;
+            const int len = (int)min((int64_t)VS, p.V - base);
+            const int len_bulk = (len * ES) / 16 * 16 / ES;
+            mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
+            if (tid == 0) stamp(j, 1);
+            uint4 raw[L][NV];
+            float tmax[L];
 #pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    const Tin* sl = ring + ((size_t)st * L + l) * VS;
+            for (int l = 0; l < L; ++l) {
+                const Tin* sl = ring + ((size_t)st * L + l) * VS;
+#pragma unroll
+                for (int jv = 0; jv < NV; ++jv) {
+                    const int e0 = (jv * CTH + tid) * VEC;
+                    if (e0 + VEC <= len_bulk) {
+                        raw[l][jv] = *reinterpret_cast<const uint4*>(sl + e0);
+                    } else {   // ragged end of the row: element-wise from smem / global
+                        const Tin* g = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
+                                       i * p.lv.ld[l] + base;
+                        Tin xs[VEC];
+#pragma unroll
+                        for (int k = 0; k < VEC; ++k) {
+                            const int ee = e0 + k;
+                            Tin z = (Tin)(-INFINITY);
+                            if (ee < len_bulk) z = sl[ee];
+                            else if (ee < len) z = g[ee];
+                            xs[k] = z;
+                        }
+                        raw[l][jv] = *reinterpret_cast<const uint4*>(xs);
+                    }
+                }
+                float tm = -INFINITY;
+                if (ES == 2) {
+                    uint32_t mx = 0xFF80FF80u;
 #pragma unroll
                     for (int jv = 0; jv < NV; ++jv) {
-                        const int e0 = (jv * CTH + tid) * VEC;
-                        if (e0 + VEC <= len_bulk) {
-                            raw[l][jv] = *reinterpret_cast<const uint4*>(sl + e0);
-                        } else {   // ragged end of the row: element-wise from smem / global
-                            const Tin* g = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
-                                           i * p.lv.ld[l] + base;
-                            Tin xs[VEC];
-#pragma unroll
-                            for (int k = 0; k < VEC; ++k) {
-                                const int ee = e0 + k;
-                                Tin z = (Tin)(-INFINITY);
-                                if (ee < len_bulk) z = sl[ee];
-                                else if (ee < len) z = g[ee];
-                                xs[k] = z;
-                            }
-                            raw[l][jv] = *reinterpret_cast<const uint4*>(xs);
-                        }
-                    }
-                    float tm;
-                    if (ES == 2) {
-                        uint4& r = raw[l][0];
+                        uint4& r = raw[l][jv];
                         r.x = clamp_bf16x2(r.x); r.y = clamp_bf16x2(r.y);
                         r.z = clamp_bf16x2(r.z); r.w = clamp_bf16x2(r.w);
-                        const uint32_t mx = max_nan_bf16x2(max_nan_bf16x2(r.x, r.y), max_nan_bf16x2(r.z, r.w));
-                        tm = fmaxf(bf16lo(mx), bf16hi(mx));
-                    } else {
-                        tm = -INFINITY;
-#pragma unroll
-                        for (int jv = 0; jv < NV; ++jv) {
-                            float xs[4];
-                            unpack_clamped<float>(raw[l][jv], xs);
-                            raw[l][jv] = make_uint4(__float_as_uint(xs[0]), __float_as_uint(xs[1]),
-                                                    __float_as_uint(xs[2]), __float_as_uint(xs[3]));
-                            tm = fmaxf(tm, fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])));
-                        }
+                        mx = max_nan_bf16x2(mx, max_nan_bf16x2(max_nan_bf16x2(r.x, r.y), max_nan_bf16x2(r.z, r.w)));
                     }
-                    tmax[l] = tm;
-                }
-                // per-warp max of all rows, the shuffle chains interleaved
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                    for (int l = 0; l < L; ++l) tmax[l] = fmaxf(tmax[l], __shfl_xor_sync(0xffffffffu, tmax[l], o));
-                }
-                if (lane == 0) {
-#pragma unroll
-                    for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
-                }
-                float Sv[L], Kv[L];
-                int am[L];
-                float xprev[CET];
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    float x[CET];
+                    tm = fmaxf(bf16lo(mx), bf16hi(mx));
+                } else {
 #pragma unroll
                     for (int jv = 0; jv < NV; ++jv) {
-                        const uint4 r = raw[l][jv];
-                        if (ES == 2) {
-                            x[0] = bf16lo(r.x); x[1] = bf16hi(r.x); x[2] = bf16lo(r.y); x[3] = bf16hi(r.y);
-                            x[4] = bf16lo(r.z); x[5] = bf16hi(r.z); x[6] = bf16lo(r.w); x[7] = bf16hi(r.w);
-                        } else {
-                            x[(jv * 4 + 0) % CET] = __uint_as_float(r.x); x[(jv * 4 + 1) % CET] = __uint_as_float(r.y);
-                            x[(jv * 4 + 2) % CET] = __uint_as_float(r.z); x[(jv * 4 + 3) % CET] = __uint_as_float(r.w);
-                        }
+                        float xs[4];
+                        unpack_clamped<float>(raw[l][jv], xs);
+                        raw[l][jv] = make_uint4(__float_as_uint(xs[0]), __float_as_uint(xs[1]),
+                                                __float_as_uint(xs[2]), __float_as_uint(xs[3]));
+                        tm = fmaxf(tm, fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])));
                     }
-                    const float m = tmax[l];
-                    const float shift = l > 0 ? m - tmax[l > 0 ? l - 1 : 0] : 0.f;
-                    float e[CET];
-                    float sum = 0.f, ks = 0.f;
-#pragma unroll
-                    for (int k = 0; k < CET; ++k) {
-                        e[k] = ex2f((x[k] - m) * LOG2E);
-                        sum += e[k];
-                        if (l > 0) ks = fmaf(e[k], (x[k] - xprev[k]) - shift, ks);
-                    }
-                    tm_st8(tbase + (uint32_t)(q * CET * L + l * CET), e);
-                    Sv[l] = sum;
-                    Kv[l] = ks;
-                    am[l] = 0x7fffffff;
-                    if (GREEDY) {
-#pragma unroll
-                        for (int k = CET - 1; k >= 0; --k)
-                            if (x[k] == m) am[l] = (int)(base + ((k / VEC) * CTH + tid) * VEC + (k % VEC));
-                    }
-#pragma unroll
-                    for (int k = 0; k < CET; ++k) xprev[k] = x[k];
                 }
+                tmax[l] = tm;
+            }
+            // per-warp max of all rows, the shuffle chains interleaved
 #pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    Sv[l] = fold4(Sv[l]);
-                    if (l > 0) Kv[l] = fold4(Kv[l]);
+            for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) tmax[l] = fmaxf(tmax[l], __shfl_xor_sync(0xffffffffu, tmax[l], o));
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
+            }
+            if (j >= NR) {   // the TMEM slot must have been read by the pass-2 warps
+                mbar_wait(&c.tm_empty[q], (uint32_t)(((j / NR) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            float Sv[L], Kv[L];
+            int am[L];
+            float xprev[CET];
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                float x[CET];
+#pragma unroll
+                for (int jv = 0; jv < NV; ++jv) {
+                    const uint4 r = raw[l][jv];
+                    if (ES == 2) {
+                        x[jv * 8 + 0] = bf16lo(r.x); x[jv * 8 + 1] = bf16hi(r.x);
+                        x[jv * 8 + 2] = bf16lo(r.y); x[jv * 8 + 3] = bf16hi(r.y);
+                        x[jv * 8 + 4] = bf16lo(r.z); x[jv * 8 + 5] = bf16hi(r.z);
+                        x[jv * 8 + 6] = bf16lo(r.w); x[jv * 8 + 7] = bf16hi(r.w);
+                    } else {
+                        x[(jv * 4 + 0) % CET] = __uint_as_float(r.x); x[(jv * 4 + 1) % CET] = __uint_as_float(r.y);
+                        x[(jv * 4 + 2) % CET] = __uint_as_float(r.z); x[(jv * 4 + 3) % CET] = __uint_as_float(r.w);
+                    }
                 }
+                const float m = tmax[l];
+                const float shift = l > 0 ? m - tmax[l > 0 ? l - 1 : 0] : 0.f;
+                float e[CET];
+                float sum = 0.f, ks = 0.f;
+#pragma unroll
+                for (int k = 0; k < CET; ++k) {
+                    e[k] = ex2f((x[k] - m) * LOG2E);
+                    sum += e[k];
+                    if (l > 0) ks = fmaf(e[k], (x[k] - xprev[k]) - shift, ks);
+                }
+                tm_st16(tbase + (uint32_t)(q * CET * L + l * CET), e);
+                Sv[l] = sum;
+                Kv[l] = ks;
+                am[l] = 0x7fffffff;
                 if (GREEDY) {
 #pragma unroll
-                    for (int l = 0; l < L; ++l) am[l] = warp_min_i(am[l]);
+                    for (int k = CET - 1; k >= 0; --k)
+                        if (x[k] == m) am[l] = (int)(base + ((k / VEC) * CTH + tid) * VEC + (k % VEC));
                 }
-                if (j >= R1) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
-                if (lane < NSUB) {
 #pragma unroll
-                    for (int l = 0; l < L; ++l) {
-                        c.r1S[r1][l][warp][lane] = Sv[l];
-                        c.r1K[r1][l][warp][lane] = Kv[l];
-                    }
-                    if (GREEDY && lane == 0) {
+                for (int k = 0; k < CET; ++k) xprev[k] = x[k];
+            }
 #pragma unroll
-                        for (int l = 0; l < L; ++l) c.r1A[r1][l][warp] = am[l];
-                    }
+            for (int l = 0; l < L; ++l) {
+                Sv[l] = fold4(Sv[l]);
+                if (l > 0) Kv[l] = fold4(Kv[l]);
+            }
+            if (GREEDY) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) am[l] = warp_min_i(am[l]);
+            }
+            if (j >= R1) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
+            if (lane < NSUB) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    c.r1S[r1][l][warp][lane] = Sv[l];
+                    c.r1K[r1][l][warp][lane] = Kv[l];
                 }
-                tm_wait_st();
-                __syncwarp();
-                if (tid == 0) stamp(j, 2);
-                if (lane == 0) {
-                    mbar_arrive(&c.empty[st]);
-                    mbar_arrive(&c.r1_full[r1]);
+                if (GREEDY && lane == 0) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) c.r1A[r1][l][warp] = am[l];
                 }
             }
-            if (j >= LAG) {
-                // ---- pass 2 of item j2 = j - LAG
-                const int64_t j2 = j - LAG;
-                const int q2 = (int)(j2 % NR);
-                const int r2 = (int)(j2 % R2);
-                mbar_wait(&c.rowf_full[q2], (uint32_t)((j2 / NR) & 1));
-                if (tid == 0) stamp(j2, 6);
-                float rh[L], rl[L];
-                double sc[L];
-#pragma unroll
-                for (int l = 1; l < L; ++l) {
-                    rh[l] = c.rowf[q2][l][warp].rho_hi;
-                    rl[l] = c.rowf[q2][l][warp].rho_lo;
-                    sc[l] = c.rowf[q2][l][warp].scale;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&c.rowf_empty[q2]);
-                float ev[L][CET];
-#pragma unroll
-                for (int l = 0; l < L; ++l) tm_ld8(tbase + (uint32_t)(q2 * CET * L + l * CET), ev[l]);
-                tm_wait_ld();
-                float acc[L];
-#pragma unroll
-                for (int l = 1; l < L; ++l) {
-                    float a = 0.f;
-#pragma unroll
-                    for (int k = 0; k < CET; ++k) {
-                        float t = fmaf(-ev[l - 1][k], rh[l], ev[l][k]);
-                        t = fmaf(-ev[l - 1][k], rl[l], t);
-                        a += fmaxf(t, 0.f);
-                    }
-                    acc[l] = a;
-                }
-#pragma unroll
-                for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
-                if (j2 >= R2) mbar_wait(&c.r2_empty[r2], (uint32_t)(((j2 / R2) - 1) & 1));
-                if (lane < NSUB) {
-#pragma unroll
-                    for (int l = 1; l < L; ++l) c.r2R[r2][l][warp][lane] = acc[l];
-                }
-                if (lane == 0) {
-#pragma unroll
-                    for (int l = 1; l < L; ++l) c.r2scale[r2][l][warp] = sc[l];
-                }
-                __syncwarp();
-                if (tid == 0) stamp(j2, 7);
-                if (lane == 0) mbar_arrive(&c.r2_full[r2]);
+            tm_wait_st();
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (tid == 0) stamp(j, 2);
+            if (lane == 0) {
+                mbar_arrive(&c.empty[st]);
+                mbar_arrive(&c.r1_full[r1]);
+                mbar_arrive(&c.tm_full[q]);
             }
+        }
+    } else if (warp < W_PROD) {
+        // ================================================================ pass-2 warps
+        // warp NCW + w reads the TMEM lanes / columns written by pass-1 warp w
+        const int w = warp - W_P2;
+        const uint32_t tbase = c.taddr + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((w >> 2) * 256);
+        for (int64_t j = 0; j < n_my; ++j) {
+            const int q = (int)(j % NR);
+            const int r2 = (int)(j % R2);
+            mbar_wait(&c.rowf_full[q], (uint32_t)((j / NR) & 1));
+            if (w == 0 && lane == 0) stamp(j, 6);
+            float rh[L], rl[L];
+            double sc[L];
+#pragma unroll
+            for (int l = 1; l < L; ++l) {
+                rh[l] = c.rowf[q][l][w].rho_hi;
+                rl[l] = c.rowf[q][l][w].rho_lo;
+                sc[l] = c.rowf[q][l][w].scale;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c.rowf_empty[q]);
+            mbar_wait(&c.tm_full[q], (uint32_t)((j / NR) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            float ev[L][CET];
+#pragma unroll
+            for (int l = 0; l < L; ++l) tm_ld16(tbase + (uint32_t)(q * CET * L + l * CET), ev[l]);
+            tm_wait_ld();
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c.tm_empty[q]);
+            float acc[L];
+#pragma unroll
+            for (int l = 1; l < L; ++l) {
+                float a = 0.f;
+#pragma unroll
+                for (int k = 0; k < CET; ++k) {
+                    float t = fmaf(-ev[l - 1][k], rh[l], ev[l][k]);
+                    t = fmaf(-ev[l - 1][k], rl[l], t);
+                    a += fmaxf(t, 0.f);
+                }
+                acc[l] = a;
+            }
+#pragma unroll
+            for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
+            if (j >= R2) mbar_wait(&c.r2_empty[r2], (uint32_t)(((j / R2) - 1) & 1));
+            if (lane < NSUB) {
+#pragma unroll
+                for (int l = 1; l < L; ++l) c.r2R[r2][l][w][lane] = acc[l];
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int l = 1; l < L; ++l) c.r2scale[r2][l][w] = sc[l];
+            }
+            __syncwarp();
+            if (w == 0 && lane == 0) stamp(j, 7);
+            if (lane == 0) mbar_arrive(&c.r2_full[r2]);
         }
     } else if (warp == W_PROD) {
         // ================================================================ TMA producer
@@ -364,8 +402,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
     } else if (warp == W_PUB) {
         // ================================================================ publisher
-        // lane = 2 * w + h: warp w, half h of its NSUB records
-        const int w = lane >> 1, h = lane & 1;
+        // lane = 4 * w + t: pass-1 warp w, record t (of NSUB)
+        const int w = lane >> 2, t = lane & 3;
         for (int64_t j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
@@ -377,16 +415,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             int aw[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                float a = 0.f, k = 0.f;
-#pragma unroll
-                for (int t = 0; t < NSUB / 2; ++t) {
-                    a += c.r1S[r1][l][w][h * (NSUB / 2) + t];
-                    k += c.r1K[r1][l][w][h * (NSUB / 2) + t];
-                }
-                Sw[l] = a + __shfl_xor_sync(0xffffffffu, a, 1);
-                Kw[l] = k + __shfl_xor_sync(0xffffffffu, k, 1);
+                Sw[l] = c.r1S[r1][l][w][t];
+                Kw[l] = c.r1K[r1][l][w][t];
                 wm[l] = c.wmx[q][l][w];
-                aw[l] = GREEDY ? c.r1A[r1][l][w] : 0x7fffffff;
+                aw[l] = (GREEDY && t == 0) ? c.r1A[r1][l][w] : 0x7fffffff;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
@@ -396,19 +428,19 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             for (int l = 0; l < L; ++l) {
                 float ms = wm[l];
 #pragma unroll
-                for (int o = 16; o > 1; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+                for (int o = 16; o > 2; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
                 double f = exp((double)wm[l] - (double)ms);
                 if (!(wm[l] > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;   // fully masked warp
-                double Sd = h == 0 ? (double)Sw[l] * f : 0.0;
+                double Sd = (double)Sw[l] * f;
                 double Kd = 0.0;
-                if (h == 0 && l > 0 && f != 0.0)   // restore the per-warp KL shift in float64
+                if (l > 0 && f != 0.0)   // restore the per-warp KL shift in float64
                     Kd = ((double)Kw[l] + ((double)wm[l] - (double)wm[l > 0 ? l - 1 : 0]) * (double)Sw[l]) * f;
-                int a = (h == 0 && wm[l] == ms) ? aw[l] : 0x7fffffff;
+                int a = (wm[l] == ms) ? aw[l] : 0x7fffffff;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
                     Sd += __shfl_xor_sync(0xffffffffu, Sd, o);
-                    Kd += __shfl_xor_sync(0xffffffffu, Kd, o);
-                    a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+                    if (l > 0) Kd += __shfl_xor_sync(0xffffffffu, Kd, o);
+                    if (GREEDY) a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
                 }
                 const float Sf = (float)Sd;
                 rec[l] = ((unsigned long long)__float_as_uint(Sf) << 32) | __float_as_uint(ms);
@@ -486,26 +518,26 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 }
                 Sl[l] = warp_sum_d(Sx);
             }
-            // per-warp factors: lane handles compute warp (lane & 15) for rows of parity (lane >> 4)
+            // per-warp factors: lane = 8 (l - 1) + w for pass-1 warp w and the pair ending at row l
             if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
-            const int w = lane & 15;
-            double cl[L];
+            {
+                const int w = lane & 7, l = 1 + (lane >> 3);
+                if (l < L) {
+                    double Ma = Ml[0], Mb = Ml[0], Sa = Sl[0], Sb = Sl[0];
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                const float wm = c.wmx[q][l][w];
-                cl[l] = (wm > NEG_MASKED && Ml[l] > NEG_MASKED) ? exp((double)wm - Ml[l]) : 0.0;
-            }
-#pragma unroll
-            for (int l = 1; l < L; ++l) {
-                if ((l & 1) != (lane >> 4)) continue;
-                const bool skip = !(cl[l] > 0.0) || !(Sl[l] > 0.0) || !(Sl[l - 1] > 0.0) || !isfinite(Sl[l]) ||
-                                  !isfinite(Sl[l - 1]);
-                const double rho = skip ? 0.0 : cl[l - 1] * Sl[l] / (Sl[l - 1] * cl[l]);
-                WF wf;
-                wf.rho_hi = skip ? 0.f : (float)rho;
-                wf.rho_lo = skip ? 0.f : (float)(rho - (double)wf.rho_hi);
-                wf.scale = skip ? 0.0 : cl[l] / Sl[l];
-                c.rowf[q][l][w] = wf;
+                    for (int r = 1; r < L; ++r)
+                        if (r == l) { Ma = Ml[r]; Sa = Sl[r]; Mb = Ml[r - 1]; Sb = Sl[r - 1]; }
+                    const float wa = c.wmx[q][l][w], wb = c.wmx[q][l - 1][w];
+                    const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? exp((double)wa - Ma) : 0.0;
+                    const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp((double)wb - Mb) : 0.0;
+                    const bool skip = !(ca > 0.0) || !(Sa > 0.0) || !(Sb > 0.0) || !isfinite(Sa) || !isfinite(Sb);
+                    const double rho = skip ? 0.0 : cb * Sa / (Sb * ca);
+                    WF wf;
+                    wf.rho_hi = skip ? 0.f : (float)rho;
+                    wf.rho_lo = skip ? 0.f : (float)(rho - (double)wf.rho_hi);
+                    wf.scale = skip ? 0.0 : ca / Sa;
+                    c.rowf[q][l][w] = wf;
+                }
             }
             __syncwarp();
             if (lane == 0) {
@@ -515,7 +547,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
     } else if (warp == W_RED) {
         // ================================================================ reducer (slice residual)
-        const int w = lane >> 1, h = lane & 1;
+        const int w = lane >> 2, t = lane & 3;
         for (int64_t j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
@@ -525,10 +557,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             double R[L];
 #pragma unroll
             for (int l = 1; l < L; ++l) {
-                float a = 0.f;
-#pragma unroll
-                for (int t = 0; t < NSUB / 2; ++t) a += c.r2R[r2][l][w][h * (NSUB / 2) + t];
-                double d = (double)a * c.r2scale[r2][l][w];
+                double d = (double)c.r2R[r2][l][w][t] * c.r2scale[r2][l][w];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 R[l] = d;
