@@ -212,8 +212,12 @@ __device__ __forceinline__ int warp_min_i(int v) {
 }
 
 // Combine C slice partials of one row into its RowStat (fixed order -> every CTA
-// that does it gets bit-identical results).  Executed by one full warp.
-__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out) {
+// that does it gets bit-identical results).  Executed by one full warp.  If `prev`
+// (the previous level's partials of the same slices) is given, the slice KL numerators
+// are stored relative to the slice shift m_s - m'_s and that shift is restored here in
+// float64: K = sum_s (K_s + (m_s - m'_s) S_s) e^{m_s - M}.
+__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out,
+                                      const Partial* prev = nullptr) {
     const int lane = threadIdx.x & 31;
     float m = -INFINITY;
     for (int s = lane; s < C; s += 32) m = fmaxf(m, __ldcg(&parts[s].m));
@@ -227,6 +231,7 @@ __device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out
         double Ks = __ldcg(&parts[s].Kl);
         double f = exp((double)ms - (double)m);
         S += Ss * f;
+        if (prev) Ks += ((double)ms - (double)__ldcg(&prev[s].m)) * Ss;
         Kl += Ks * f;
         if (ms == m) am = min(am, __ldcg(&parts[s].amax));
         if (isnan(ms) || isnan(Ss)) bad = true;

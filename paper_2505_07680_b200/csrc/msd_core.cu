@@ -240,13 +240,13 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) tmax[l] = fmaxf(tmax[l], __shfl_xor_sync(0xffffffffu, tmax[l], o));
             }
+            if (j >= NR) {   // slot q (TMEM and wmx) must have been released by the pass-2 warps
+                mbar_wait(&c.tm_empty[q], (uint32_t)(((j / NR) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
             if (lane == 0) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
-            }
-            if (j >= NR) {   // the TMEM slot must have been read by the pass-2 warps
-                mbar_wait(&c.tm_empty[q], (uint32_t)(((j / NR) - 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             }
             float Sv[L], Kv[L];
             int am[L];
@@ -422,32 +422,48 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
+            // slice combine in fp32 (per-warp factors on the MUFU); the KL numerator is kept
+            // relative to the slice shift sigma = m_s,l - m_s,l-1 (restored in float64 by the tail)
             unsigned long long rec[L];
             Partial pr[L];
+            float msl[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
                 float ms = wm[l];
 #pragma unroll
                 for (int o = 16; o > 2; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-                double f = exp((double)wm[l] - (double)ms);
-                if (!(wm[l] > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;   // fully masked warp
-                double Sd = (double)Sw[l] * f;
-                double Kd = 0.0;
-                if (l > 0 && f != 0.0)   // restore the per-warp KL shift in float64
-                    Kd = ((double)Kw[l] + ((double)wm[l] - (double)wm[l > 0 ? l - 1 : 0]) * (double)Sw[l]) * f;
-                int a = (wm[l] == ms) ? aw[l] : 0x7fffffff;
+                msl[l] = ms;
+            }
+            float Sx[L], Kx[L];
+            int ax[L];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    Sd += __shfl_xor_sync(0xffffffffu, Sd, o);
-                    if (l > 0) Kd += __shfl_xor_sync(0xffffffffu, Kd, o);
-                    if (GREEDY) a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+            for (int l = 0; l < L; ++l) {
+                float f = ex2f((wm[l] - msl[l]) * LOG2E);
+                if (!(wm[l] > NEG_MASKED)) f = (msl[l] > NEG_MASKED) ? 0.f : 1.f;   // fully masked warp
+                Sx[l] = Sw[l] * f;
+                Kx[l] = 0.f;
+                if (l > 0 && f != 0.f) {
+                    const float dsh = (wm[l] - wm[l > 0 ? l - 1 : 0]) - (msl[l] - msl[l > 0 ? l - 1 : 0]);
+                    Kx[l] = f * fmaf(dsh, Sw[l], Kw[l]);
                 }
-                const float Sf = (float)Sd;
-                rec[l] = ((unsigned long long)__float_as_uint(Sf) << 32) | __float_as_uint(ms);
-                pr[l].m = ms;
-                pr[l].amax = a;
-                pr[l].S = Sd;
-                pr[l].Kl = Kd;
+                ax[l] = (wm[l] == msl[l]) ? aw[l] : 0x7fffffff;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    Sx[l] += __shfl_xor_sync(0xffffffffu, Sx[l], o);
+                    if (l > 0) Kx[l] += __shfl_xor_sync(0xffffffffu, Kx[l], o);
+                    if (GREEDY) ax[l] = min(ax[l], __shfl_xor_sync(0xffffffffu, ax[l], o));
+                }
+            }
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                rec[l] = ((unsigned long long)__float_as_uint(Sx[l]) << 32) | __float_as_uint(msl[l]);
+                pr[l].m = msl[l];
+                pr[l].amax = ax[l];
+                pr[l].S = (double)Sx[l];
+                pr[l].Kl = (double)Kx[l];      // relative to the slice shift (see the tail)
             }
             if (lane < L) {
                 const size_t idx = ((size_t)u * L + lane) * C + s;

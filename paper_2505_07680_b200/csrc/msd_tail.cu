@@ -384,7 +384,8 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
     for (int r = warp; r < K * L; r += NWARP) {
         const int i = r / L, l = r % L;
         double Kl;
-        RowStat rs = combine_row(p.partials + (((size_t)b * K + i) * L + l) * C, C, &Kl);
+        const Partial* pp = p.partials + (((size_t)b * K + i) * L + l) * C;
+        RowStat rs = combine_row(pp, C, &Kl, l > 0 ? pp - C : nullptr);
         if (lane == 0) { sh.row[i][l] = rs; sh.kl[i][l] = Kl; }
     }
     __syncthreads();
