@@ -229,7 +229,7 @@ const char* msd_last_error(void);
 int32_t msd_abi_version(void);
 msd_status msd_prof_enable(int32_t on);
 msd_status msd_prof_read(double* core_ms, int32_t* core_launches, int32_t* total_launches);
-/* msd_debug_set_trace: device buffer of 64 bytes per core item (unit x slice) receiving 8
+/* msd_debug_set_trace: device buffer of 128 bytes per core item (unit x slice) receiving 16
  * globaltimer stamps of the pipeline stages of each item (NULL disables).  Debug only. */
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes);
 

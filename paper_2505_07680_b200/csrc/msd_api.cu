@@ -322,7 +322,7 @@ msd_status msd_kv_rollback(const msd_paged_kv* kv, int32_t n_models, int32_t B,
 
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes) {
     g_trace = reinterpret_cast<unsigned long long*>(dev_buf);
-    g_trace_items = dev_buf ? bytes / 64 : 0;
+    g_trace_items = dev_buf ? bytes / 128 : 0;
     return MSD_OK;
 }
 

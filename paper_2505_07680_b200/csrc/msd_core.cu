@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     auto stamp = [&](int64_t j, int k) {
-        if (p.trace) p.trace[(blockIdx.x + j * G) * 8 + k] = globaltimer();
+        if (p.trace) p.trace[(blockIdx.x + j * G) * 16 + k] = globaltimer();
     };
     auto item = [&](int64_t j, int64_t& u, int& s, int64_t& b, int64_t& i) {
         const int64_t w = blockIdx.x + j * G;
@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 mbar_wait(&c.tm_empty[q], (uint32_t)(((j / NR) - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             }
+            if (tid == 0) stamp(j, 2);
             if (lane == 0) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             tm_wait_st();
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
-            if (tid == 0) stamp(j, 2);
+            if (tid == 0) stamp(j, 3);
             if (lane == 0) {
                 mbar_arrive(&c.empty[st]);
                 mbar_arrive(&c.r1_full[r1]);
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int q = (int)(j % NR);
             const int r2 = (int)(j % R2);
             mbar_wait(&c.rowf_full[q], (uint32_t)((j / NR) & 1));
-            if (w == 0 && lane == 0) stamp(j, 6);
+            if (w == 0 && lane == 0) stamp(j, 11);
             float rh[L], rl[L];
             double sc[L];
 #pragma unroll
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.rowf_empty[q]);
             mbar_wait(&c.tm_full[q], (uint32_t)((j / NR) & 1));
+            if (w == 0 && lane == 0) stamp(j, 12);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float ev[L][CET];
 #pragma unroll
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 for (int l = 1; l < L; ++l) c.r2scale[r2][l][w] = sc[l];
             }
             __syncwarp();
-            if (w == 0 && lane == 0) stamp(j, 7);
+            if (w == 0 && lane == 0) stamp(j, 13);
             if (lane == 0) mbar_arrive(&c.r2_full[r2]);
         }
     } else if (warp == W_PROD) {
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int q = (int)(j % NR);
             const int r1 = (int)(j % R1);
             mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
+            if (lane == 0) stamp(j, 4);
             float Sw[L], Kw[L], wm[L];
             int aw[L];
 #pragma unroll
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             __syncwarp();
             if (lane == 0) {
                 red_add_relaxed(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
-                stamp(j, 3);
+                stamp(j, 5);
             }
         }
     } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
@@ -492,6 +495,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             item(j, u, s, b, i);
             const int q = (int)(j % NR);
             const uint64_t t0 = globaltimer();
+            if (lane == 0) stamp(j, 6);
             if (lane == 0) {
                 while (ld_relaxed_u32(&p.cnt[(size_t)u * CNT_STRIDE]) < (uint32_t)C) {
                     __nanosleep(100);
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 }
             }
             __syncwarp();
-            if (lane == 0) stamp(j, 4);
+            if (lane == 0) stamp(j, 7);
             // stage the unit's records; a record whose sum is still 0 is not yet visible
             const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
             while (true) {
@@ -535,7 +539,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 Sl[l] = warp_sum_d(Sx);
             }
             // per-warp factors: lane = 8 (l - 1) + w for pass-1 warp w and the pair ending at row l
+            if (lane == 0) stamp(j, 8);
             if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
+            if (lane == 0) stamp(j, 9);
             {
                 const int w = lane & 7, l = 1 + (lane >> 3);
                 if (l < L) {
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             }
             __syncwarp();
             if (lane == 0) {
-                stamp(j, 5);
+                stamp(j, 10);
                 mbar_arrive(&c.rowf_full[q]);
             }
         }
@@ -570,6 +576,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             item(j, u, s, b, i);
             const int r2 = (int)(j % R2);
             mbar_wait(&c.r2_full[r2], (uint32_t)((j / R2) & 1));
+            if (lane == 0) stamp(j, 14);
             double R[L];
 #pragma unroll
             for (int l = 1; l < L; ++l) {
@@ -587,6 +594,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     if (lane == l) v = R[l];
                 p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = v;
             }
+            if (lane == 0) stamp(j, 15);
         }
     }
 

@@ -1,4 +1,4 @@
-"""Run a workload once with the core-kernel stage trace and summarise latencies."""
+"""Run a workload once with the core-kernel stage trace (16 stamps / item) and summarise."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -9,30 +9,36 @@ inp = synth.gauss_chain(c["B"], c["V"], c["K"], c["L"], c["sigmas"], s=c["s"], s
 cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"])
 C = (c["V"] + 4095) // 4096
 n_items = c["B"] * c["K"] * C
-buf = torch.zeros(n_items * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(n_items * 16, dtype=torch.int64, device="cuda")
 lib = api.lib(); lib.msd_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 cv(); torch.cuda.synchronize()
 lib.msd_debug_set_trace(buf.data_ptr(), buf.numel() * 8)
 cv(); torch.cuda.synchronize()
 lib.msd_debug_set_trace(None, 0)
-t = buf.view(n_items, 8).cpu().numpy().astype(np.float64)
+t = buf.view(n_items, 16).cpu().numpy().astype(np.float64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan) / 1e3   # us
-names = ["tma_issue", "p1_start", "p1_end", "published", "cnt_seen", "rowf_ready", "p2_start", "p2_end"]
-print("kernel span us", np.nanmax(t))
-for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 6), (6, 7), (2, 6)]:
-    d = t[:, b] - t[:, a]
-    print(f"{names[a]:>10} -> {names[b]:<10} median {np.nanmedian(d):8.2f}  p90 {np.nanpercentile(d, 90):8.2f}  max {np.nanmax(d):8.2f}")
-G = 148
-p1 = t[:, 1]
-cta = np.arange(n_items) % G
-for g in (0, 1, 77, 147):
-    s = p1[cta == g]
-    print("cta", g, "items", s.size, "p1-start spacing median", np.nanmedian(np.diff(s)), "first", np.round(s[:6], 2))
+N = ["tma", "p1.full", "p1.tmE", "p1.end", "pub.r1", "pub.done", "f.start", "f.cnt", "f.comb", "f.rowfE",
+     "f.done", "p2.rowf", "p2.tmF", "p2.end", "red.r2", "red.end"]
+print("kernel span us %.1f" % np.nanmax(t))
+def d(a, b):
+    x = t[:, b] - t[:, a]
+    return f"{N[a]:>8} -> {N[b]:<8} med {np.nanmedian(x):7.2f} p90 {np.nanpercentile(x, 90):7.2f}"
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (6, 7), (7, 8), (8, 9), (9, 10), (10, 11), (11, 12), (12, 13), (13, 14), (14, 15), (5, 7)]:
+    print(d(a, b))
 U = n_items // C
-pub = t[:, 3].reshape(U, C)
-print("unit publish spread (max-min) median", np.nanmedian(np.nanmax(pub, 1) - np.nanmin(pub, 1)),
-      "p90", np.nanpercentile(np.nanmax(pub, 1) - np.nanmin(pub, 1), 90))
-lastpub = np.repeat(np.nanmax(pub, 1), C)
-print("cnt_seen - last publish median", np.nanmedian(t[:, 4] - lastpub), "p90", np.nanpercentile(t[:, 4] - lastpub, 90))
-print("p1_start(j) spacing global median (all ctas)", np.nanmedian(np.diff(np.sort(p1))))
+pub = t[:, 5].reshape(U, C)
+last = np.repeat(np.nanmax(pub, 1), C)
+print("last publish -> cnt seen  med %.2f p90 %.2f" % (np.nanmedian(t[:, 7] - last), np.nanpercentile(t[:, 7] - last, 90)))
+print("unit publish spread med %.2f" % np.nanmedian(np.nanmax(pub, 1) - np.nanmin(pub, 1)))
+G = 148
+cta = np.arange(n_items) % G
+for g in (0, 100):
+    sel = cta == g
+    for k in (1, 3, 5, 10, 13):
+        print(f"cta {g} {N[k]:>8} spacing med {np.nanmedian(np.diff(t[sel, k])):6.2f}", end=";")
+    print()
+# who is last in each unit: distribution of CTA index of the last publisher
+lastc = np.nanargmax(pub, 1)
+print("fraction of units whose last slice is the straddling (next-round) part:",
+      np.mean([(np.arange(u * C, u * C + C) // G).max() != (u * C) // G for u in range(U)]))
