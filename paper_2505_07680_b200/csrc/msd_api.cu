@@ -135,7 +135,7 @@ msd_status run_engine(const Engine& E) {
     memset(&cp, 0, sizeof(cp));
     cp.lv = E.lv;
     cp.L = E.L; cp.B = E.B; cp.K = E.K; cp.V = E.V;
-    cp.C = w.C; cp.U = w.U;
+    cp.C = w.C; cp.U = w.U; cp.VSe = slice_geometry(E.V).VSe;
     cp.n_items = (int64_t)w.U * w.C;
     cp.partials = reinterpret_cast<Partial*>(ws + w.partials);
     cp.partms = reinterpret_cast<float2*>(ws + w.partms);
@@ -151,7 +151,7 @@ msd_status run_engine(const Engine& E) {
     TailParams tp;
     memset(&tp, 0, sizeof(tp));
     tp.lv = E.lv;
-    tp.L = E.L; tp.B = E.B; tp.K = E.K; tp.C = w.C; tp.V = E.V;
+    tp.L = E.L; tp.B = E.B; tp.K = E.K; tp.C = w.C; tp.V = E.V; tp.VSe = cp.VSe;
     tp.cand0 = E.cand0; tp.m0 = E.m0;
     tp.u_acc = E.u_acc; tp.u_emit = E.u_emit;
     tp.ua_l = E.ua_l; tp.ua_b = E.ua_b; tp.ue_l = E.ue_l; tp.ue_b = E.ue_b;

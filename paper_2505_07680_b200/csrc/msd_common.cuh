@@ -44,6 +44,28 @@ struct RowStat {
     int32_t bad;    // NaN / +inf present or row all -inf
 };
 
+// Slice geometry of a vocabulary of V entries: C slices of VSe (<= VS) entries.  C is
+// the smallest value in [ceil(V/VS), 2 ceil(V/VS)] for which k = floor(148/C) groups of C
+// CTAs keep >= 144 SMs busy (a group owns whole units, so units never straddle rounds and
+// the groups never wait on each other; see msd_core.cu).
+struct SliceGeom {
+    int32_t C;
+    int32_t VSe;
+};
+constexpr int REF_SMS = 148;   // B200
+__host__ __device__ inline SliceGeom slice_geometry(int64_t V) {
+    const int32_t cmin = (int32_t)((V + VS - 1) / VS);
+    int32_t best = cmin, used = (REF_SMS / cmin) * cmin;
+    for (int32_t c = cmin + 1; c <= 2 * cmin && c <= REF_SMS && used < REF_SMS - 4; ++c) {
+        const int32_t u = (REF_SMS / c) * c;   // smallest C that keeps >= 144 of 148 SMs busy
+        if (u > used) { used = u; best = c; }
+    }
+    SliceGeom g;
+    g.C = best;
+    g.VSe = (int32_t)(((V + best - 1) / best + 7) / 8 * 8);
+    return g;
+}
+
 // Workspace layout (bytes), shared by host and device code.
 struct WsLayout {
     size_t hdr, cnt, ready, partials, partms, rowstat, kl, resid, total;
@@ -57,7 +79,7 @@ __host__ __device__ inline WsLayout ws_layout(int32_t L, int32_t B, int32_t K, i
     WsLayout w;
     w.L = L;
     w.U = B * K;
-    w.C = (int32_t)ceil_div(V, VS);
+    w.C = slice_geometry(V).C;
     size_t off = 0;
     w.hdr = off;      off += 256;
     // one counter per 256-byte block: concurrent units' counters must not share an L2 line
@@ -209,6 +231,31 @@ __device__ __forceinline__ int warp_min_i(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+}
+
+// exp(x) in float64 for x <= 0, branch-free apart from underflow (relative error ~1e-13):
+// 2^(x log2 e) = 2^n * e^(f ln 2), f in [0,1), degree-13 Taylor polynomial of e^t.
+__device__ __forceinline__ double dexp_neg(double x) {
+    if (!(x > -700.0)) return 0.0;
+    const double y = x * 1.4426950408889634074;
+    const double n = floor(y);
+    const double t = (y - n) * 0.69314718055994530942;
+    double r = 1.6059043836821614599e-10;          // 1/13!
+    r = fma(r, t, 2.0876756987868098979e-09);      // 1/12!
+    r = fma(r, t, 2.5052108385441718775e-08);
+    r = fma(r, t, 2.7557319223985890653e-07);
+    r = fma(r, t, 2.7557319223985890653e-06);
+    r = fma(r, t, 2.4801587301587301587e-05);
+    r = fma(r, t, 1.9841269841269841270e-04);
+    r = fma(r, t, 1.3888888888888888889e-03);
+    r = fma(r, t, 8.3333333333333333333e-03);
+    r = fma(r, t, 4.1666666666666666667e-02);
+    r = fma(r, t, 1.6666666666666666667e-01);
+    r = fma(r, t, 0.5);
+    r = fma(r, t, 1.0);
+    r = fma(r, t, 1.0);
+    const long long e = (long long)n;
+    return r * __longlong_as_double((e + 1023) << 52);
 }
 
 // Combine C slice partials of one row into its RowStat (fixed order -> every CTA

@@ -135,9 +135,13 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     Ctl<L>& c = *reinterpret_cast<Ctl<L>*>(smem + align_up((size_t)S * L * VS * ES, 128));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t G = gridDim.x;
-    const int64_t n_my = p.n_items > (int64_t)blockIdx.x ? (p.n_items - blockIdx.x + G - 1) / G : 0;
     const int C = p.C;
+    const int VSe = p.VSe;
+    // group scheduling: the grid is k groups of C CTAs; CTA (group, s) handles slice s of
+    // units group, group + k, ... -- a unit's C slices always run together on one group
+    const int kgrp = gridDim.x / C;
+    const int grp = blockIdx.x / C, sfix = blockIdx.x % C;
+    const int64_t n_my = grp < kgrp && grp < p.U ? ((int64_t)p.U - grp + kgrp - 1) / kgrp : 0;
 
     if (warp == W_PROD) {
         if (lane == 0) {
@@ -161,12 +165,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     auto stamp = [&](int64_t j, int k) {
-        if (p.trace) p.trace[(blockIdx.x + j * G) * 16 + k] = globaltimer();
+        if (p.trace) p.trace[((grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
     };
     auto item = [&](int64_t j, int64_t& u, int& s, int64_t& b, int64_t& i) {
-        const int64_t w = blockIdx.x + j * G;
-        u = w / C;
-        s = (int)(w % C);
+        u = grp + j * kgrp;
+        s = sfix;
         b = u / p.K;
         i = u % p.K;
     };
@@ -181,8 +184,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int st = (int)(j % S);
             const int q = (int)(j % NR);
             const int r1 = (int)(j % R1);
-            const int64_t base = (int64_t)s * VS;
-            const int len = (int)min((int64_t)VS, p.V - base);
+            const int64_t base = (int64_t)s * VSe;
+            const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
             const int len_bulk = (len * ES) / 16 * 16 / ES;
             mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
             if (tid == 0) stamp(j, 1);
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 int64_t u, b, i;
                 int s;
                 item(j, u, s, b, i);
-                const int64_t len = min((int64_t)VS, p.V - (int64_t)s * VS);
+                const int64_t len = max((int64_t)0, min((int64_t)VSe, p.V - (int64_t)s * VSe));
                 const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
                 stamp(j, 0);
                 mbar_arrive_expect_tx(&c.full[st], bytes * L);
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
-                                         i * p.lv.ld[l] + (int64_t)s * VS;
+                                         i * p.lv.ld[l] + (int64_t)s * VSe;
                         bulk_g2s(ring + ((size_t)st * L + l) * VS, src, bytes, &c.full[st], pol);
                     }
                 }
@@ -524,19 +527,40 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 __nanosleep(64);
             }
             __syncwarp();
+            // row normalisers from the C slice records: all L rows interleaved (float64 sums)
             double Ml[L], Sl[L];
+            {
+                float m[L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                float m = -INFINITY;
-                for (int t = lane; t < C; t += 32) m = fmaxf(m, __uint_as_float((uint32_t)fb[l * C + t]));
-                Ml[l] = (double)warp_max(m);
-                double Sx = 0.0;
+                for (int l = 0; l < L; ++l) m[l] = -INFINITY;
                 for (int t = lane; t < C; t += 32) {
-                    const unsigned long long r = fb[l * C + t];
-                    const float vm = __uint_as_float((uint32_t)r);
-                    if (vm > NEG_MASKED) Sx += (double)__uint_as_float((uint32_t)(r >> 32)) * exp((double)vm - Ml[l]);
+#pragma unroll
+                    for (int l = 0; l < L; ++l) m[l] = fmaxf(m[l], __uint_as_float((uint32_t)fb[l * C + t]));
                 }
-                Sl[l] = warp_sum_d(Sx);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) m[l] = fmaxf(m[l], __shfl_xor_sync(0xffffffffu, m[l], o));
+                }
+                double sx[L];
+#pragma unroll
+                for (int l = 0; l < L; ++l) { Ml[l] = (double)m[l]; sx[l] = 0.0; }
+                for (int t = lane; t < C; t += 32) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        const unsigned long long r = fb[l * C + t];
+                        const float vm = __uint_as_float((uint32_t)r);
+                        if (vm > NEG_MASKED)
+                            sx[l] += (double)__uint_as_float((uint32_t)(r >> 32)) * dexp_neg((double)vm - Ml[l]);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) sx[l] += __shfl_xor_sync(0xffffffffu, sx[l], o);
+                }
+#pragma unroll
+                for (int l = 0; l < L; ++l) Sl[l] = sx[l];
             }
             // per-warp factors: lane = 8 (l - 1) + w for pass-1 warp w and the pair ending at row l
             if (lane == 0) stamp(j, 8);
@@ -550,8 +574,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     for (int r = 1; r < L; ++r)
                         if (r == l) { Ma = Ml[r]; Sa = Sl[r]; Mb = Ml[r - 1]; Sb = Sl[r - 1]; }
                     const float wa = c.wmx[q][l][w], wb = c.wmx[q][l - 1][w];
-                    const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? exp((double)wa - Ma) : 0.0;
-                    const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp((double)wb - Mb) : 0.0;
+                    const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? dexp_neg((double)wa - Ma) : 0.0;
+                    const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? dexp_neg((double)wb - Mb) : 0.0;
                     const bool skip = !(ca > 0.0) || !(Sa > 0.0) || !(Sb > 0.0) || !isfinite(Sa) || !isfinite(Sb);
                     const double rho = skip ? 0.0 : cb * Sa / (Sb * ca);
                     WF wf;
@@ -623,9 +647,11 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, CORE_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
-    int64_t grid = nsm;                    // one CTA per SM (it owns all 512 TMEM columns)
-    if (grid > p.n_items) grid = p.n_items;
-    if (grid < p.C && grid < p.n_items) return cudaErrorInvalidConfiguration;
+    // one CTA per SM (it owns all 512 TMEM columns); k = floor(nsm / C) groups of C CTAs
+    int64_t kg = nsm / p.C;
+    if (kg < 1) return cudaErrorInvalidConfiguration;
+    if (kg > p.U) kg = p.U;
+    const int64_t grid = kg * p.C;
     void* args[] = {&p};
     return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(CORE_THREADS), args, smem, s);
 }

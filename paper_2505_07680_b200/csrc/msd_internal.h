@@ -21,7 +21,7 @@ struct LevelDesc {
 
 struct CoreParams {
     LevelDesc lv;
-    int32_t L, B, K, C, U;
+    int32_t L, B, K, C, U, VSe;
     int64_t V;
     int64_t n_items;
     int32_t stages;
@@ -39,7 +39,7 @@ struct CoreParams {
 
 struct TailParams {
     LevelDesc lv;
-    int32_t L, B, K, C;
+    int32_t L, B, K, C, VSe;
     int64_t V;
     const int32_t* cand0;
     const int32_t* m0;

@@ -86,10 +86,11 @@ __device__ __forceinline__ float block_max_f(float v, TailShared& sh) {
 // Load this thread's ET elements of slice s of a row (same mapping as the core),
 // clamped; out-of-row entries are NEG_CLAMP.
 template <typename Tin>
-__device__ __forceinline__ void load_slice(const Tin* row, int64_t V, int s, float* x) {
+__device__ __forceinline__ void load_slice(const Tin* row, int64_t V, int s, int vse, float* x) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NV = ET / VEC;
-    const int64_t base = (int64_t)s * VS;
+    const int64_t base = (int64_t)s * vse;
+    V = min(V, base + vse);           // the slice ends at the next slice's start
 #pragma unroll
     for (int jv = 0; jv < NV; ++jv) {
         const int64_t e0 = base + (jv * T + threadIdx.x) * VEC;
@@ -107,14 +108,14 @@ __device__ __forceinline__ void load_slice(const Tin* row, int64_t V, int s, flo
 // Row statistics of an arbitrary row (bonus rows at positions >= K): per-slice
 // partials into sh.part[], combined RowStat returned to every thread.
 template <typename Tin>
-__device__ RowStat row_stats(const Tin* row, int64_t V, int C, TailShared& sh) {
+__device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShared& sh) {
     constexpr int VEC = Elem<Tin>::VEC;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ float wmx[NWARP], wsm[NWARP];
     __shared__ int wam[NWARP];
     for (int s = 0; s < C; ++s) {
         float x[ET];
-        load_slice<Tin>(row, V, s, x);
+        load_slice<Tin>(row, V, s, vse, x);
         float tm = x[0];
 #pragma unroll
         for (int k = 1; k < ET; ++k) tm = fmaxf(tm, x[k]);
@@ -126,7 +127,7 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, TailShared& sh) {
         int am = 0x7fffffff;
 #pragma unroll
         for (int k = ET - 1; k >= 0; --k)
-            if (x[k] == wm) am = (int)((int64_t)s * VS + ((k / VEC) * T + threadIdx.x) * VEC + (k % VEC));
+            if (x[k] == wm) am = (int)((int64_t)s * vse + ((k / VEC) * T + threadIdx.x) * VEC + (k % VEC));
         am = warp_min_i(am);
         __syncthreads();
         if (lane == 0) { wmx[warp] = wm; wsm[warp] = sum; wam[warp] = am; }
@@ -184,14 +185,14 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, TailShared& sh) {
 // sh.w[] (fp32 per element, float64 across warps; the core's pass-2 arithmetic).
 template <typename Tin>
 __device__ void pair_resid(const Tin* ra, const Tin* rb, const RowStat& A, const RowStat& Bq,
-                           int64_t V, int C, TailShared& sh) {
+                           int64_t V, int C, int vse, TailShared& sh) {
     const double rho = Bq.S > 0 ? A.S / Bq.S : 0.0;
     const float rh = (float)rho, rl = (float)(rho - (double)rh);
     const float Ma = (float)A.M, Mb = (float)Bq.M;
     for (int s = 0; s < C; ++s) {
         float xa[ET], xb[ET];
-        load_slice<Tin>(ra, V, s, xa);
-        load_slice<Tin>(rb, V, s, xb);
+        load_slice<Tin>(ra, V, s, vse, xa);
+        load_slice<Tin>(rb, V, s, vse, xb);
         float acc = 0.f;
 #pragma unroll
         for (int k = 0; k < ET; ++k) {
@@ -222,9 +223,10 @@ __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, d
 // contiguous entries [t*16, t*16+16) of the slice.  Returns the token or -1.
 template <typename Tin>
 __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A, double B,
-                              int64_t V, int s, double before, double target, double Z, double u,
+                              int64_t V, int s, int vse, double before, double target, double Z, double u,
                               TailShared& sh, bool* tie) {
-    const int64_t e0 = (int64_t)s * VS + threadIdx.x * ET;
+    const int64_t e0 = (int64_t)s * vse + threadIdx.x * ET;
+    V = min(V, (int64_t)(s + 1) * vse);
     if (threadIdx.x == 0) sh.near = 0;
     double w[ET];
     double loc = 0.0;
@@ -278,9 +280,9 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
 // Last entry with positive weight in slice s (clamp rule, reading R5).
 template <typename Tin>
 __device__ int32_t last_positive(bool resid, const Tin* ra, const Tin* rb, double A, double B,
-                                 int64_t V, int s, TailShared& sh) {
+                                 int64_t V, int s, int vse, TailShared& sh) {
     int best = -1;
-    for (int64_t v = (int64_t)s * VS + threadIdx.x; v < min(V, (int64_t)(s + 1) * VS); v += T) {
+    for (int64_t v = (int64_t)s * vse + threadIdx.x; v < min(V, (int64_t)(s + 1) * vse); v += T) {
         const float za = clamp1(Elem<Tin>::load1(ra + v));
         const float zb = resid ? clamp1(Elem<Tin>::load1(rb + v)) : NEG_CLAMP;
         if (wt(resid, za, zb, A, B) > 0.0) best = max(best, (int)v);
@@ -292,7 +294,7 @@ __device__ int32_t last_positive(bool resid, const Tin* ra, const Tin* rb, doubl
 // prefix, rescan it.  Returns token or -1 (inconsistent -> caller goes exact).
 template <typename Tin>
 __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double A, double B,
-                               int64_t V, int C, double Z, double u, TailShared& sh, bool* tie) {
+                               int64_t V, int C, int vse, double Z, double u, TailShared& sh, bool* tie) {
     if (threadIdx.x == 0) {
         const double target = u * Z;
         double c = 0.0;
@@ -314,16 +316,16 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
     __syncthreads();
     if (sel < 0) {  // u*Z beyond the total (rounding): clamp to the last positive entry
         *tie = true;
-        return last_positive<Tin>(resid, ra, rb, A, B, V, -1 - sel, sh);
+        return last_positive<Tin>(resid, ra, rb, A, B, V, -1 - sel, vse, sh);
     }
-    return scan_slice<Tin>(resid, ra, rb, A, B, V, sel, before, u * Z, Z, u, sh, tie);
+    return scan_slice<Tin>(resid, ra, rb, A, B, V, sel, vse, before, u * Z, Z, u, sh, tie);
 }
 
 // Exact float64 draw over the whole row (pair): exact normalisers, exact slice
 // masses, exact scan.  Residual mass < 1e-12 -> draw from p.
 template <typename Tin>
 __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const RowStat& Ar,
-                              const RowStat& Br, int64_t V, int C, double u, TailShared& sh,
+                              const RowStat& Br, int64_t V, int C, int vse, double u, TailShared& sh,
                               bool* tie, bool* small) {
   for (int attempt = 0; attempt < 2; ++attempt) {
     // exact normalisers
@@ -342,7 +344,7 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
     const double B = resid ? Br.M + log(sb) : 0.0;
     for (int s = 0; s < C; ++s) {
         double acc = 0.0;
-        for (int64_t v = (int64_t)s * VS + threadIdx.x; v < min(V, (int64_t)(s + 1) * VS); v += T) {
+        for (int64_t v = (int64_t)s * vse + threadIdx.x; v < min(V, (int64_t)(s + 1) * vse); v += T) {
             const float za = clamp1(Elem<Tin>::load1(ra + v));
             const float zb = resid ? clamp1(Elem<Tin>::load1(rb + v)) : NEG_CLAMP;
             acc += wt(resid, za, zb, A, B);
@@ -358,7 +360,7 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
         resid = false;
         continue;
     }
-    int32_t y = draw_slices<Tin>(resid, ra, rb, A, B, V, C, Z, u, sh, tie);
+    int32_t y = draw_slices<Tin>(resid, ra, rb, A, B, V, C, vse, Z, u, sh, tie);
     return y < 0 ? 0 : y;
   }
   return 0;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         for (int i = K; i < m; ++i) {
             for (int lv = l - 1; lv <= l; ++lv) {
                 if (!sh.extra_ok[lv][i - K]) {
-                    RowStat r = row_stats<Tin>(row_ptr<Tin>(p, lv, b, i), V, C, sh);
+                    RowStat r = row_stats<Tin>(row_ptr<Tin>(p, lv, b, i), V, C, p.VSe, sh);
                     if (tid == 0) { sh.extra[lv][i - K] = r; sh.extra_ok[lv][i - K] = 1; }
                     __syncthreads();
                 }
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
                 Bq = sh.row[pos][l - 1];
             } else {
                 if (!resid) {  // bonus row: (re)compute so sh.part holds its slice partials
-                    RowStat r = row_stats<Tin>(ra, V, C, sh);
+                    RowStat r = row_stats<Tin>(ra, V, C, p.VSe, sh);
                     if (tid == 0) { sh.extra[l][pos - K] = r; sh.extra_ok[l][pos - K] = 1; }
                     __syncthreads();
                 }
@@ -518,7 +520,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
                         for (int s = tid; s < C; s += T) sh.w[s] = R[s];
                         __syncthreads();
                     } else {
-                        pair_resid<Tin>(ra, rb, A, Bq, V, C, sh);
+                        pair_resid<Tin>(ra, rb, A, Bq, V, C, p.VSe, sh);
                     }
                 } else {
                     const Partial* P = p.partials + (((size_t)b * K + pos) * L + l) * C;
@@ -532,11 +534,11 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
                 for (int s = 0; s < C; ++s) Z += sh.w[s];
                 y = -1;
                 if (!p.exact_all && (!resid || Z >= p.z_safe))
-                    y = draw_slices<Tin>(resid, ra, rb, A.lse, Bq.lse, V, C, Z, u, sh, &tie);
+                    y = draw_slices<Tin>(resid, ra, rb, A.lse, Bq.lse, V, C, p.VSe, Z, u, sh, &tie);
                 if (y < 0) {
                     exact = true;
                     tie = false;
-                    y = draw_exact<Tin>(resid, ra, rb, A, Bq, V, C, u, sh, &tie, &small);
+                    y = draw_exact<Tin>(resid, ra, rb, A, Bq, V, C, p.VSe, u, sh, &tie, &small);
                 }
             }
             if (tid == 0) {
