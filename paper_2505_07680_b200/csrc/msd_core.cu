@@ -81,6 +81,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
     return r;
 }
+// relaxed load without a compiler memory clobber: independent loads stay in flight together
+__device__ __forceinline__ unsigned long long ld_relaxed_u64_nc(const unsigned long long* p) {
+    unsigned long long r;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -199,7 +205,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const int e0 = (jv * CTH + tid) * VEC;
                     if (e0 + VEC <= len_bulk) {
                         raw[l][jv] = *reinterpret_cast<const uint4*>(sl + e0);
-                    } else {   // ragged end of the row: element-wise from smem / global
+                    } else if (e0 >= len) {   // past the end of this slice: all -inf
+                        if (ES == 2) raw[l][jv] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+                        else raw[l][jv] = make_uint4(0xFF800000u, 0xFF800000u, 0xFF800000u, 0xFF800000u);
+                    } else {   // the vector straddling the end of the row: element-wise
                         const Tin* g = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
                                        i * p.lv.ld[l] + base;
                         Tin xs[VEC];
@@ -510,11 +519,20 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             // stage the unit's records; a record whose sum is still 0 is not yet visible
             const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
             while (true) {
+                // all loads in flight before any use (one round trip), then stage in smem
+                constexpr int MAXB = (MAXL * 128 + 31) / 32;
+                unsigned long long rr[MAXB];
+#pragma unroll
+                for (int t = 0; t < MAXB; ++t) {
+                    const int idx = t * 32 + lane;
+                    rr[t] = idx < LC ? ld_relaxed_u64_nc(pm + idx) : 0x100000000ull;
+                }
                 bool ok = true;
-                for (int idx = lane; idx < LC; idx += 32) {
-                    const unsigned long long r = ld_relaxed_u64(pm + idx);
-                    fb[idx] = r;
-                    ok &= (uint32_t)(r >> 32) != 0u;
+#pragma unroll
+                for (int t = 0; t < MAXB; ++t) {
+                    const int idx = t * 32 + lane;
+                    if (idx < LC) fb[idx] = rr[t];
+                    ok &= (uint32_t)(rr[t] >> 32) != 0u;
                 }
                 if (__all_sync(0xffffffffu, ok)) break;
                 if (globaltimer() - t0 > 4000000000ull) {

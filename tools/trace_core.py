@@ -7,7 +7,14 @@ name = sys.argv[1] if len(sys.argv) > 1 else "llama3"
 c = synth.CONFIGS[name]
 inp = synth.gauss_chain(c["B"], c["V"], c["K"], c["L"], c["sigmas"], s=c["s"], seed=c["seed"], device="cuda", dtype=c["dtype"])
 cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"])
-C = (c["V"] + 4095) // 4096
+def geo(V, VS=4096, REF=148):
+    cmin = (V + VS - 1) // VS; best = cmin; used = (REF // cmin) * cmin; cc = cmin + 1
+    while cc <= 2 * cmin and cc <= REF and used < REF - 4:
+        u = (REF // cc) * cc
+        if u > used: used = u; best = cc
+        cc += 1
+    return best
+C = geo(c["V"])
 n_items = c["B"] * c["K"] * C
 buf = torch.zeros(n_items * 16, dtype=torch.int64, device="cuda")
 lib = api.lib(); lib.msd_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
@@ -31,8 +38,11 @@ pub = t[:, 5].reshape(U, C)
 last = np.repeat(np.nanmax(pub, 1), C)
 print("last publish -> cnt seen  med %.2f p90 %.2f" % (np.nanmedian(t[:, 7] - last), np.nanpercentile(t[:, 7] - last, 90)))
 print("unit publish spread med %.2f" % np.nanmedian(np.nanmax(pub, 1) - np.nanmin(pub, 1)))
-G = 148
-cta = np.arange(n_items) % G
+G = (148 // C) * C
+kg = G // C
+uu = np.arange(n_items) // C
+ss = np.arange(n_items) % C
+cta = (uu % kg) * C + ss
 for g in (0, 100):
     sel = cta == g
     for k in (1, 3, 5, 10, 13):
@@ -40,5 +50,4 @@ for g in (0, 100):
     print()
 # who is last in each unit: distribution of CTA index of the last publisher
 lastc = np.nanargmax(pub, 1)
-print("fraction of units whose last slice is the straddling (next-round) part:",
-      np.mean([(np.arange(u * C, u * C + C) // G).max() != (u * C) // G for u in range(U)]))
+print("C", C, "groups", kg)
