@@ -68,8 +68,8 @@ struct Ctl {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void red_add_relaxed(uint32_t* p, uint32_t v) {
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
     uint32_t r;
@@ -480,19 +480,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 pr[l].S = (double)Sx[l];
                 pr[l].Kl = (double)Kx[l];      // relative to the slice shift (see the tail)
             }
-            if (lane < L) {
-                const size_t idx = ((size_t)u * L + lane) * C + s;
-                unsigned long long rv = rec[0];
-                Partial pv = pr[0];
-#pragma unroll
-                for (int l = 1; l < L; ++l)
-                    if (lane == l) { rv = rec[l]; pv = pr[l]; }
-                p.partials[idx] = pv;
-                st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx, rv);
-            }
-            __syncwarp();
+            // lane 0 issues every record store and then the counter increment with release
+            // semantics, so a fetcher that sees the count complete sees every record
             if (lane == 0) {
-                red_add_relaxed(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    const size_t idx = ((size_t)u * L + l) * C + s;
+                    p.partials[idx] = pr[l];
+                    st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx, rec[l]);
+                }
+                red_add_release(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
                 stamp(j, 5);
             }
         }
@@ -514,6 +511,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     if (globaltimer() - t0 > 4000000000ull) break;
                 }
             }
+            if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
             __syncwarp();
             if (lane == 0) stamp(j, 7);
             // stage the unit's records; a record whose sum is still 0 is not yet visible
