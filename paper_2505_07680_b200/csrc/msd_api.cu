@@ -136,6 +136,8 @@ msd_status run_engine(const Engine& E) {
     cp.lv = E.lv;
     cp.L = E.L; cp.B = E.B; cp.K = E.K; cp.V = E.V;
     cp.C = w.C; cp.U = w.U; cp.VSe = slice_geometry(E.V).VSe;
+    cp.kinv = (uint32_t)((((uint64_t)1 << 32) + (uint64_t)E.K - 1) / (uint64_t)E.K);
+    if (w.U >= (1 << 24)) return fail(MSD_E_ARG, "B*K = %d units exceeds 2^24", w.U);
     cp.n_items = (int64_t)w.U * w.C;
     cp.partials = reinterpret_cast<Partial*>(ws + w.partials);
     cp.partms = reinterpret_cast<float2*>(ws + w.partms);

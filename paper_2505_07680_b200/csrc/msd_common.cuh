@@ -233,15 +233,17 @@ __device__ __forceinline__ int warp_min_i(int v) {
     return v;
 }
 
-// exp(x) in float64 for x <= 0, branch-free apart from underflow (relative error ~1e-13):
-// 2^(x log2 e) = 2^n * e^(f ln 2), f in [0,1), degree-13 Taylor polynomial of e^t.
+// exp(x) in float64 for x <= 0 on the FMA/ALU pipes only (no MUFU, no F2I/FRND: the
+// MUFU pipe is saturated by the streaming ex2 of the pass-1 warps).  Relative error ~2e-16.
+// 2^(x log2 e) = 2^n * e^(f ln 2), n = rint via the 1.5*2^52 magic, |f| <= 1/2.
 __device__ __forceinline__ double dexp_neg(double x) {
     if (!(x > -700.0)) return 0.0;
+    const double magic = 6755399441055744.0;
     const double y = x * 1.4426950408889634074;
-    const double n = floor(y);
-    const double t = (y - n) * 0.69314718055994530942;
-    double r = 1.6059043836821614599e-10;          // 1/13!
-    r = fma(r, t, 2.0876756987868098979e-09);      // 1/12!
+    const double ym = y + magic;
+    const double n = ym - magic;
+    const double t = (y - n) * 0.69314718055994530942;     // |t| <= 0.347
+    double r = 2.0876756987868098979e-09;                   // 1/12!
     r = fma(r, t, 2.5052108385441718775e-08);
     r = fma(r, t, 2.7557319223985890653e-07);
     r = fma(r, t, 2.7557319223985890653e-06);
@@ -254,8 +256,35 @@ __device__ __forceinline__ double dexp_neg(double x) {
     r = fma(r, t, 0.5);
     r = fma(r, t, 1.0);
     r = fma(r, t, 1.0);
-    const long long e = (long long)n;
-    return r * __longlong_as_double((e + 1023) << 52);
+    const int ni = __double2loint(ym);                      // n as a two's-complement int
+    return r * __hiloint2double((ni + 1023) << 20, 0);
+}
+
+// 1/x in float64 for x > 0 with FMA-pipe Newton iterations only (no MUFU.RCP64H).
+__device__ __forceinline__ double drcp_fma(double x) {
+    double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));   // ~10% guess
+#pragma unroll
+    for (int it = 0; it < 5; ++it) y = y * fma(-x, y, 2.0);
+    return y;
+}
+
+// 2^x in float32 for x <= 0 on the FMA/ALU pipes only (relative error ~1e-7).
+__device__ __forceinline__ float exp2f_fma(float x) {
+    if (!(x > -126.f)) return 0.f;
+    const float magic = 12582912.f;                         // 1.5 * 2^23
+    const float xm = x + magic;
+    const float n = xm - magic;
+    const float t = (x - n) * 0.69314718056f;              // |t| <= 0.347
+    float r = 1.98412698e-4f;                               // 1/7!
+    r = fmaf(r, t, 1.38888889e-3f);
+    r = fmaf(r, t, 8.33333333e-3f);
+    r = fmaf(r, t, 4.16666667e-2f);
+    r = fmaf(r, t, 1.66666667e-1f);
+    r = fmaf(r, t, 0.5f);
+    r = fmaf(r, t, 1.0f);
+    r = fmaf(r, t, 1.0f);
+    const int ni = __float_as_int(xm) - 0x4B400000;         // n
+    return r * __int_as_float((ni + 127) << 23);
 }
 
 // Combine C slice partials of one row into its RowStat (fixed order -> every CTA

@@ -128,6 +128,10 @@ __device__ __forceinline__ float fold4(float v) {
     return v;
 }
 
+__host__ __device__ constexpr int core_stages(int L, int es) {
+    return (147456 / (L * VS * es)) < 2 ? 2 : ((147456 / (L * VS * es)) > SMAX ? SMAX : (147456 / (L * VS * es)));
+}
+
 template <typename Tin, int L, bool GREEDY>
 __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
@@ -136,7 +140,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int NR = 256 / (CET * L);     // TMEM item slots (256 columns per pass-1 warp)
     static_assert(NR <= NRMAX && NR >= 2, "TMEM slots");
     extern __shared__ __align__(128) unsigned char smem[];
-    const int S = p.stages;
+    constexpr int S = core_stages(L, ES);
     Tin* ring = reinterpret_cast<Tin*>(smem);
     Ctl<L>& c = *reinterpret_cast<Ctl<L>*>(smem + align_up((size_t)S * L * VS * ES, 128));
 
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     // units group, group + k, ... -- a unit's C slices always run together on one group
     const int kgrp = gridDim.x / C;
     const int grp = blockIdx.x / C, sfix = blockIdx.x % C;
-    const int64_t n_my = grp < kgrp && grp < p.U ? ((int64_t)p.U - grp + kgrp - 1) / kgrp : 0;
+    const int n_my = grp < kgrp && grp < p.U ? (p.U - grp + kgrp - 1) / kgrp : 0;
 
     if (warp == W_PROD) {
         if (lane == 0) {
@@ -170,20 +174,23 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    auto stamp = [&](int64_t j, int k) {
-        if (p.trace) p.trace[((grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
+    auto stamp = [&](int j, int k) {
+        if (p.trace) p.trace[((int64_t)(grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
     };
-    auto item = [&](int64_t j, int64_t& u, int& s, int64_t& b, int64_t& i) {
-        u = grp + j * kgrp;
+    // (no runtime integer division on the hot loops: it would issue on the busy MUFU pipe)
+    auto item = [&](int j, int64_t& u, int& s, int64_t& b, int64_t& i) {
+        const uint32_t uu = (uint32_t)(grp + j * kgrp);
+        const uint32_t bb = __umulhi(uu, p.kinv);
+        u = uu;
         s = sfix;
-        b = u / p.K;
-        i = u % p.K;
+        b = bb;
+        i = uu - bb * (uint32_t)p.K;
     };
 
     if (warp < NCW) {
         // ================================================================ pass-1 warps
         const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
-        for (int64_t j = 0; j < n_my; ++j) {
+        for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // warp NCW + w reads the TMEM lanes / columns written by pass-1 warp w
         const int w = warp - W_P2;
         const uint32_t tbase = c.taddr + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((w >> 2) * 256);
-        for (int64_t j = 0; j < n_my; ++j) {
+        for (int j = 0; j < n_my; ++j) {
             const int q = (int)(j % NR);
             const int r2 = (int)(j % R2);
             mbar_wait(&c.rowf_full[q], (uint32_t)((j / NR) & 1));
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // ================================================================ TMA producer
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            for (int64_t j = 0; j < n_my; ++j) {
+            for (int j = 0; j < n_my; ++j) {
                 const int st = (int)(j % S);
                 if (j >= S) mbar_wait(&c.empty[st], (uint32_t)(((j / S) - 1) & 1));
                 int64_t u, b, i;
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // ================================================================ publisher
         // lane = 4 * w + t: pass-1 warp w, record t (of NSUB)
         const int w = lane >> 2, t = lane & 3;
-        for (int64_t j = 0; j < n_my; ++j) {
+        for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
@@ -453,7 +460,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             int ax[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                float f = ex2f((wm[l] - msl[l]) * LOG2E);
+                float f = exp2f_fma((wm[l] - msl[l]) * LOG2E);   // FMA pipe: MUFU is busy
                 if (!(wm[l] > NEG_MASKED)) f = (msl[l] > NEG_MASKED) ? 0.f : 1.f;   // fully masked warp
                 Sx[l] = Sw[l] * f;
                 Kx[l] = 0.f;
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         const int f = warp - W_FETCH0;
         const int LC = L * C;
         unsigned long long* fb = c.fbuf[f];
-        for (int64_t j = f; j < n_my; j += NFETCH) {
+        for (int j = f; j < n_my; j += NFETCH) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
@@ -593,11 +600,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? dexp_neg((double)wa - Ma) : 0.0;
                     const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? dexp_neg((double)wb - Mb) : 0.0;
                     const bool skip = !(ca > 0.0) || !(Sa > 0.0) || !(Sb > 0.0) || !isfinite(Sa) || !isfinite(Sb);
-                    const double rho = skip ? 0.0 : cb * Sa / (Sb * ca);
+                    const double rho = skip ? 0.0 : cb * Sa * drcp_fma(Sb * ca);
                     WF wf;
                     wf.rho_hi = skip ? 0.f : (float)rho;
                     wf.rho_lo = skip ? 0.f : (float)(rho - (double)wf.rho_hi);
-                    wf.scale = skip ? 0.0 : ca / Sa;
+                    wf.scale = skip ? 0.0 : ca * drcp_fma(Sa);
                     c.rowf[q][l][w] = wf;
                 }
             }
@@ -610,7 +617,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     } else if (warp == W_RED) {
         // ================================================================ reducer (slice residual)
         const int w = lane >> 2, t = lane & 3;
-        for (int64_t j = 0; j < n_my; ++j) {
+        for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
             item(j, u, s, b, i);
@@ -649,9 +656,7 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     CoreParams p = p0;
     const int ES = (int)sizeof(Tin);
     const size_t stage_bytes = (size_t)L * VS * ES;
-    int S = (int)(147456 / stage_bytes);
-    if (S < 2) S = 2;
-    if (S > SMAX) S = SMAX;
+    const int S = core_stages(L, ES);
     p.stages = S;
     const size_t smem = align_up(stage_bytes * S, 128) + sizeof(Ctl<L>) + 128;
     auto k = core_kernel<Tin, L, G>;

@@ -22,6 +22,7 @@ struct LevelDesc {
 struct CoreParams {
     LevelDesc lv;
     int32_t L, B, K, C, U, VSe;
+    uint32_t kinv;      // ceil(2^32 / K): u / K == umulhi(u, kinv) for u < 2^24
     int64_t V;
     int64_t n_items;
     int32_t stages;
