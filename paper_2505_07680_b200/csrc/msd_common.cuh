@@ -260,6 +260,27 @@ __device__ __forceinline__ double dexp_neg(double x) {
     return r * __hiloint2double((ni + 1023) << 20, 0);
 }
 
+// float -> double on the integer pipe (no F2F: conversions share the XU pipe with MUFU).
+// Exact for normal floats, zero and +-inf/NaN; float denormals flush to zero.
+__device__ __forceinline__ double f2d_alu(float f) {
+    const uint32_t b = __float_as_uint(f);
+    const uint32_t e = (b >> 23) & 0xffu;
+    const uint32_t sign = b & 0x80000000u;
+    if (e == 0u) return __hiloint2double((int)sign, 0);
+    const uint32_t m = b & 0x7fffffu;
+    const uint32_t e64 = (e == 0xffu) ? 0x7ffu : (e + 896u);
+    return __hiloint2double((int)(sign | (e64 << 20) | (m >> 3)), (int)(m << 29));
+}
+// double -> float by mantissa truncation on the integer pipe (normal range only); used to
+// split a double into hi + lo floats where hi + lo reproduces it to ~2^-48.
+__device__ __forceinline__ float d2f_trunc_alu(double d) {
+    const uint32_t hi = (uint32_t)__double2hiint(d), lo = (uint32_t)__double2loint(d);
+    const int e = (int)((hi >> 20) & 0x7ffu) - 1023 + 127;
+    if (e <= 0) return 0.f;
+    if (e >= 255) return __uint_as_float((hi & 0x80000000u) | 0x7f800000u);
+    return __uint_as_float((hi & 0x80000000u) | ((uint32_t)e << 23) | ((hi & 0xfffffu) << 3) | (lo >> 29));
+}
+
 // 1/x in float64 for x > 0 with FMA-pipe Newton iterations only (no MUFU.RCP64H).
 __device__ __forceinline__ double drcp_fma(double x) {
     double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));   // ~10% guess

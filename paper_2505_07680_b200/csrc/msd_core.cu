@@ -432,7 +432,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int q = (int)(j % NR);
             const int r1 = (int)(j % R1);
             mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
-            if (lane == 0) stamp(j, 4);
             float Sw[L], Kw[L], wm[L];
             int aw[L];
 #pragma unroll
@@ -484,8 +483,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 rec[l] = ((unsigned long long)__float_as_uint(Sx[l]) << 32) | __float_as_uint(msl[l]);
                 pr[l].m = msl[l];
                 pr[l].amax = ax[l];
-                pr[l].S = (double)Sx[l];
-                pr[l].Kl = (double)Kx[l];      // relative to the slice shift (see the tail)
+                pr[l].S = f2d_alu(Sx[l]);
+                pr[l].Kl = f2d_alu(Kx[l]);     // relative to the slice shift (see the tail)
             }
             // lane 0 issues every record store and then the counter increment with release
             // semantics, so a fetcher that sees the count complete sees every record
@@ -550,6 +549,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 __nanosleep(64);
             }
             __syncwarp();
+            if (lane == 0) stamp(j, 4);
             // row normalisers from the C slice records: all L rows interleaved (float64 sums)
             double Ml[L], Sl[L];
             {
@@ -567,14 +567,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 }
                 double sx[L];
 #pragma unroll
-                for (int l = 0; l < L; ++l) { Ml[l] = (double)m[l]; sx[l] = 0.0; }
+                for (int l = 0; l < L; ++l) { Ml[l] = f2d_alu(m[l]); sx[l] = 0.0; }
                 for (int t = lane; t < C; t += 32) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         const unsigned long long r = fb[l * C + t];
                         const float vm = __uint_as_float((uint32_t)r);
                         if (vm > NEG_MASKED)
-                            sx[l] += (double)__uint_as_float((uint32_t)(r >> 32)) * dexp_neg((double)vm - Ml[l]);
+                            sx[l] += f2d_alu(__uint_as_float((uint32_t)(r >> 32))) * dexp_neg(f2d_alu(vm) - Ml[l]);
                     }
                 }
 #pragma unroll
@@ -597,13 +597,13 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     for (int r = 1; r < L; ++r)
                         if (r == l) { Ma = Ml[r]; Sa = Sl[r]; Mb = Ml[r - 1]; Sb = Sl[r - 1]; }
                     const float wa = c.wmx[q][l][w], wb = c.wmx[q][l - 1][w];
-                    const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? dexp_neg((double)wa - Ma) : 0.0;
-                    const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? dexp_neg((double)wb - Mb) : 0.0;
+                    const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? dexp_neg(f2d_alu(wa) - Ma) : 0.0;
+                    const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? dexp_neg(f2d_alu(wb) - Mb) : 0.0;
                     const bool skip = !(ca > 0.0) || !(Sa > 0.0) || !(Sb > 0.0) || !isfinite(Sa) || !isfinite(Sb);
                     const double rho = skip ? 0.0 : cb * Sa * drcp_fma(Sb * ca);
                     WF wf;
-                    wf.rho_hi = skip ? 0.f : (float)rho;
-                    wf.rho_lo = skip ? 0.f : (float)(rho - (double)wf.rho_hi);
+                    wf.rho_hi = skip ? 0.f : d2f_trunc_alu(rho);
+                    wf.rho_lo = skip ? 0.f : d2f_trunc_alu(rho - f2d_alu(wf.rho_hi));
                     wf.scale = skip ? 0.0 : ca * drcp_fma(Sa);
                     c.rowf[q][l][w] = wf;
                 }
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             double R[L];
 #pragma unroll
             for (int l = 1; l < L; ++l) {
-                double d = (double)c.r2R[r2][l][w][t] * c.r2scale[r2][l][w];
+                double d = f2d_alu(c.r2R[r2][l][w][t]) * c.r2scale[r2][l][w];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 R[l] = d;
