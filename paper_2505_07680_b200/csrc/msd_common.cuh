@@ -289,6 +289,14 @@ __device__ __forceinline__ double drcp_fma(double x) {
     return y;
 }
 
+// 1/x in float32 (x > 0, normal) with FMA-pipe Newton iterations only (no MUFU.RCP).
+__device__ __forceinline__ float frcp_fma(float x) {
+    float y = __int_as_float(0x7EF311C3 - __float_as_int(x));   // ~12% initial guess
+#pragma unroll
+    for (int it = 0; it < 4; ++it) y = y * fmaf(-x, y, 2.0f);
+    return y;
+}
+
 // 2^x in float32 for x <= 0 on the FMA/ALU pipes only (relative error ~1e-7).
 __device__ __forceinline__ float exp2f_fma(float x) {
     if (!(x > -126.f)) return 0.f;

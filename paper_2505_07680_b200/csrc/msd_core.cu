@@ -45,8 +45,8 @@ constexpr int NSUB = 4;                // per-warp records after a 3-step shuffl
 static_assert(CET == 16, "two 16-byte bf16 vectors per thread and row");
 
 struct WF {                // pass-2 factors of one (row, warp) of the current slice
-    float rho_hi, rho_lo;  // rho = c_b S_a / (S_b c_a)  (pair ending at this row)
-    double scale;          // c_a / S_a
+    float rho;             // rho = c_b S_a / (S_b c_a)  (pair ending at this row)
+    float scale;           // c_a / S_a
 };
 template <int L>
 struct Ctl {
@@ -61,7 +61,7 @@ struct Ctl {
     int r1A[R1][L][NCW];                    // greedy: first argmax index per warp
     WF rowf[NRMAX][L][NCW];
     float r2R[R2][L][NCW][NSUB];            // pass-2 residual partials
-    double r2scale[R2][L][NCW];
+    float r2scale[R2][L][NCW];
     unsigned long long fbuf[NFETCH][MAXL * 128];   // fetcher staging of a unit's records
 };
 
@@ -350,12 +350,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int r2 = (int)(j % R2);
             mbar_wait(&c.rowf_full[q], (uint32_t)((j / NR) & 1));
             if (w == 0 && lane == 0) stamp(j, 11);
-            float rh[L], rl[L];
-            double sc[L];
+            float rh[L], sc[L];
 #pragma unroll
             for (int l = 1; l < L; ++l) {
-                rh[l] = c.rowf[q][l][w].rho_hi;
-                rl[l] = c.rowf[q][l][w].rho_lo;
+                rh[l] = c.rowf[q][l][w].rho;
                 sc[l] = c.rowf[q][l][w].scale;
             }
             __syncwarp();
@@ -376,9 +374,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 float a = 0.f;
 #pragma unroll
                 for (int k = 0; k < CET; ++k) {
-                    float t = fmaf(-ev[l - 1][k], rh[l], ev[l][k]);
-                    t = fmaf(-ev[l - 1][k], rl[l], t);
-                    a += fmaxf(t, 0.f);
+                    a += fmaxf(fmaf(-ev[l - 1][k], rh[l], ev[l][k]), 0.f);
                 }
                 acc[l] = a;
             }
@@ -550,40 +546,37 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             }
             __syncwarp();
             if (lane == 0) stamp(j, 4);
-            // row normalisers from the C slice records: all L rows interleaved (float64 sums)
-            double Ml[L], Sl[L];
+            // row normalisers from the C slice records, all L rows interleaved.  fp32 on the
+            // FMA pipe: the slice sums are fp32-accurate already and FP64 is slow on this part.
+            float Ml[L], Sl[L];
             {
-                float m[L];
 #pragma unroll
-                for (int l = 0; l < L; ++l) m[l] = -INFINITY;
+                for (int l = 0; l < L; ++l) Ml[l] = -INFINITY;
                 for (int t = lane; t < C; t += 32) {
 #pragma unroll
-                    for (int l = 0; l < L; ++l) m[l] = fmaxf(m[l], __uint_as_float((uint32_t)fb[l * C + t]));
+                    for (int l = 0; l < L; ++l) Ml[l] = fmaxf(Ml[l], __uint_as_float((uint32_t)fb[l * C + t]));
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-                    for (int l = 0; l < L; ++l) m[l] = fmaxf(m[l], __shfl_xor_sync(0xffffffffu, m[l], o));
+                    for (int l = 0; l < L; ++l) Ml[l] = fmaxf(Ml[l], __shfl_xor_sync(0xffffffffu, Ml[l], o));
                 }
-                double sx[L];
 #pragma unroll
-                for (int l = 0; l < L; ++l) { Ml[l] = f2d_alu(m[l]); sx[l] = 0.0; }
+                for (int l = 0; l < L; ++l) Sl[l] = 0.f;
                 for (int t = lane; t < C; t += 32) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         const unsigned long long r = fb[l * C + t];
                         const float vm = __uint_as_float((uint32_t)r);
                         if (vm > NEG_MASKED)
-                            sx[l] += f2d_alu(__uint_as_float((uint32_t)(r >> 32))) * dexp_neg(f2d_alu(vm) - Ml[l]);
+                            Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma((vm - Ml[l]) * LOG2E), Sl[l]);
                     }
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
-                    for (int l = 0; l < L; ++l) sx[l] += __shfl_xor_sync(0xffffffffu, sx[l], o);
+                    for (int l = 0; l < L; ++l) Sl[l] += __shfl_xor_sync(0xffffffffu, Sl[l], o);
                 }
-#pragma unroll
-                for (int l = 0; l < L; ++l) Sl[l] = sx[l];
             }
             // per-warp factors: lane = 8 (l - 1) + w for pass-1 warp w and the pair ending at row l
             if (lane == 0) stamp(j, 8);
@@ -592,19 +585,17 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             {
                 const int w = lane & 7, l = 1 + (lane >> 3);
                 if (l < L) {
-                    double Ma = Ml[0], Mb = Ml[0], Sa = Sl[0], Sb = Sl[0];
+                    float Ma = Ml[0], Mb = Ml[0], Sa = Sl[0], Sb = Sl[0];
 #pragma unroll
                     for (int r = 1; r < L; ++r)
                         if (r == l) { Ma = Ml[r]; Sa = Sl[r]; Mb = Ml[r - 1]; Sb = Sl[r - 1]; }
                     const float wa = c.wmx[q][l][w], wb = c.wmx[q][l - 1][w];
-                    const double ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? dexp_neg(f2d_alu(wa) - Ma) : 0.0;
-                    const double cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? dexp_neg(f2d_alu(wb) - Mb) : 0.0;
-                    const bool skip = !(ca > 0.0) || !(Sa > 0.0) || !(Sb > 0.0) || !isfinite(Sa) || !isfinite(Sb);
-                    const double rho = skip ? 0.0 : cb * Sa * drcp_fma(Sb * ca);
+                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? exp2f_fma((wa - Ma) * LOG2E) : 0.f;
+                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp2f_fma((wb - Mb) * LOG2E) : 0.f;
+                    const bool skip = !(ca > 0.f) || !(Sa > 0.f) || !(Sb > 0.f) || !isfinite(Sa) || !isfinite(Sb);
                     WF wf;
-                    wf.rho_hi = skip ? 0.f : d2f_trunc_alu(rho);
-                    wf.rho_lo = skip ? 0.f : d2f_trunc_alu(rho - f2d_alu(wf.rho_hi));
-                    wf.scale = skip ? 0.0 : ca * drcp_fma(Sa);
+                    wf.rho = skip ? 0.f : (cb * Sa) * frcp_fma(Sb * ca);
+                    wf.scale = skip ? 0.f : ca * frcp_fma(Sa);
                     c.rowf[q][l][w] = wf;
                 }
             }
@@ -624,10 +615,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int r2 = (int)(j % R2);
             mbar_wait(&c.r2_full[r2], (uint32_t)((j / R2) & 1));
             if (lane == 0) stamp(j, 14);
-            double R[L];
+            float R[L];
 #pragma unroll
             for (int l = 1; l < L; ++l) {
-                double d = f2d_alu(c.r2R[r2][l][w][t]) * c.r2scale[r2][l][w];
+                float d = c.r2R[r2][l][w][t] * c.r2scale[r2][l][w];
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 R[l] = d;
@@ -635,11 +626,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r2_empty[r2]);
             if (lane >= 1 && lane < L) {
-                double v = R[1];
+                float v = R[1];
 #pragma unroll
                 for (int l = 2; l < L; ++l)
                     if (lane == l) v = R[l];
-                p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = v;
+                p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = f2d_alu(v);
             }
             if (lane == 0) stamp(j, 15);
         }
