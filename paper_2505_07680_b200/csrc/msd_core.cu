@@ -34,7 +34,7 @@ namespace msd {
 constexpr int NCW = 8;                 // pass-1 warps (pass-2 warps: NCW .. 2 NCW - 1)
 constexpr int CTH = NCW * 32;          // pass-1 threads
 constexpr int CET = VS / CTH;          // elements per pass-1 thread per row (16)
-constexpr int NFETCH = 3;
+constexpr int NFETCH = 5;
 constexpr int W_P2 = NCW, W_PROD = 2 * NCW, W_PUB = 2 * NCW + 1, W_FETCH0 = 2 * NCW + 2,
               W_RED = W_FETCH0 + NFETCH;
 constexpr int CORE_THREADS = (W_RED + 1) * 32;
@@ -491,7 +491,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     p.partials[idx] = pr[l];
                     st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx, rec[l]);
                 }
-                red_add_release(&p.cnt[(size_t)u * CNT_STRIDE], 1u);
                 stamp(j, 5);
             }
         }
@@ -507,14 +506,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int q = (int)(j % NR);
             const uint64_t t0 = globaltimer();
             if (lane == 0) stamp(j, 6);
-            if (lane == 0) {
-                while (ld_relaxed_u32(&p.cnt[(size_t)u * CNT_STRIDE]) < (uint32_t)C) {
-                    __nanosleep(100);
-                    if (globaltimer() - t0 > 4000000000ull) break;
-                }
-            }
-            if (lane == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            __syncwarp();
             if (lane == 0) stamp(j, 7);
             // stage the unit's records; a record whose sum is still 0 is not yet visible
             const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
@@ -542,7 +533,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     }
                     break;
                 }
-                __nanosleep(64);
+                __nanosleep(32);
             }
             __syncwarp();
             if (lane == 0) stamp(j, 4);
