@@ -31,16 +31,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libmsd.so (or libmsd_<variant>.so with extra -D defines, for A/B experiments)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libmsd_{variant}.so")
+    if not force and not variant and up_to_date():
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "static", "-o", LIB + ".tmp", *sources()]
+           "-cudart", "static", *[f"-D{d}" for d in defines], "-o", lib + ".tmp", *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd, cwd=HERE)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

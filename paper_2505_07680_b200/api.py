@@ -16,7 +16,8 @@ import torch
 from .synth import level_rows  # noqa: F401  (re-exported for callers)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmsd.so")
+# MSD_LIB selects an alternative in-tree build (A/B experiments: tools/, never the default)
+LIB_PATH = os.path.join(_HERE, os.environ.get("MSD_LIB", "libmsd.so"))
 
 MSD_STOCHASTIC, MSD_GREEDY = 0, 1
 MSD_F32, MSD_BF16 = 0, 1

@@ -149,6 +149,7 @@ msd_status run_engine(const Engine& E) {
     cp.flags = E.flags;
     cp.err = reinterpret_cast<uint32_t*>(ws + w.hdr);
     cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
+    cp.dbg = (int32_t)env_double("MSD_CORE_DBG", 0.0);
 
     TailParams tp;
     memset(&tp, 0, sizeof(tp));
@@ -213,6 +214,9 @@ msd_status msd_chain_verify(const msd_logits* levels, int32_t L, int32_t B, int3
     if (L < 2 || L > MAXL) return fail(MSD_E_ARG, "L=%d outside [2,%d]", L, MAXL);
     if (B < 0 || K < 1 || K + L > MAXC) return fail(MSD_E_ARG, "bad B=%d / K=%d (need K+L <= 32)", B, K);
     if (V < 1 || V > (int64_t)128 * VS) return fail(MSD_E_ARG, "V=%lld outside [1, 524288]", (long long)V);
+    if ((int64_t)L * slice_geometry(V).C > 192)
+        return fail(MSD_E_ARG, "L * slices = %d * %d exceeds 192 (vocabulary too large for L levels)", L,
+                    slice_geometry(V).C);
     if (mode != MSD_STOCHASTIC && mode != MSD_GREEDY) return fail(MSD_E_ARG, "unknown mode %d", mode);
     if (draft_fed < 0 || draft_fed > K) return fail(MSD_E_ARG, "draft_fed=%d outside [0,K]", draft_fed);
     if (B == 0) return MSD_OK;

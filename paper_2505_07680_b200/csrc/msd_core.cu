@@ -39,6 +39,8 @@ constexpr int W_P2 = NCW, W_PROD = 2 * NCW, W_PUB = 2 * NCW + 1, W_FETCH0 = 2 * 
               W_RED = W_FETCH0 + NFETCH;
 constexpr int CORE_THREADS = (W_RED + 1) * 32;
 constexpr int SMAX = 6;
+constexpr int FBUF = 192;              // records per fetcher staging buffer (L * C <= 192)
+constexpr int SMEM_BUDGET = 227 * 1024;
 constexpr int NRMAX = 8;
 constexpr int R1 = 3, R2 = 3;          // pass-1 / pass-2 record rings
 constexpr int NSUB = 4;                // per-warp records after a 3-step shuffle fold (lanes 0..3)
@@ -62,7 +64,7 @@ struct Ctl {
     WF rowf[NRMAX][L][NCW];
     float r2R[R2][L][NCW][NSUB];            // pass-2 residual partials
     float r2scale[R2][L][NCW];
-    unsigned long long fbuf[NFETCH][MAXL * 128];   // fetcher staging of a unit's records
+    unsigned long long fbuf[NFETCH][FBUF];       // fetcher staging of a unit's records
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -128,8 +130,89 @@ __device__ __forceinline__ float fold4(float v) {
     return v;
 }
 
+// TMA ring depth: 4 stages of 24-32 KB (bf16, L = 3-4) keep ~2 us of HBM data in flight.
+#ifndef MSD_RING_BYTES
+#define MSD_RING_BYTES 98304
+#endif
 __host__ __device__ constexpr int core_stages(int L, int es) {
-    return (147456 / (L * VS * es)) < 2 ? 2 : ((147456 / (L * VS * es)) > SMAX ? SMAX : (147456 / (L * VS * es)));
+    return (MSD_RING_BYTES / (L * VS * es)) < 2 ? 2
+         : ((MSD_RING_BYTES / (L * VS * es)) > SMAX ? SMAX : (MSD_RING_BYTES / (L * VS * es)));
+}
+// item slots of parked exponentials: TMEM holds 256 / (16 L) items per pass-1 warp; the
+// shared memory left after the ring and the control block adds 1-2 more (L = 3, 4).
+__host__ __device__ constexpr int core_tslots(int L) { return 256 / (CET * L); }
+__host__ __device__ constexpr int core_sslots_raw(int L, int es, int ctl_bytes) {
+    return (SMEM_BUDGET - core_stages(L, es) * L * VS * es - ctl_bytes - 1024) / (L * CET * CTH * 4);
+}
+#ifndef MSD_SSLOTS_MAX
+#define MSD_SSLOTS_MAX 0   // measured: parking items in shared memory costs more than it hides
+#endif
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int core_sslots(int L, int es, int ctl_bytes) {
+    return core_sslots_raw(L, es, ctl_bytes) < 0
+               ? 0
+               : cmin(cmin(core_sslots_raw(L, es, ctl_bytes), MSD_SSLOTS_MAX), NRMAX - core_tslots(L));
+}
+
+// elements (2 pp, 2 pp + 1) of a thread's 16-byte vector as a float pair
+template <typename Tin>
+__device__ __forceinline__ float2 elem_pair(const uint4& r, int pp);
+template <>
+__device__ __forceinline__ float2 elem_pair<__nv_bfloat16>(const uint4& r, int pp) {
+    const uint32_t w = pp == 0 ? r.x : pp == 1 ? r.y : pp == 2 ? r.z : r.w;
+    return make_float2(bf16lo(w), bf16hi(w));
+}
+template <>
+__device__ __forceinline__ float2 elem_pair<float>(const uint4& r, int pp) {
+    return pp == 0 ? make_float2(__uint_as_float(r.x), __uint_as_float(r.y))
+                   : make_float2(__uint_as_float(r.z), __uint_as_float(r.w));
+}
+
+// The VEC-element vector that straddles the end of a row: the bulk-copied part from shared
+// memory, the tail (< 16 bytes) from global memory, -inf past the row.  Out of line so the
+// pass-1 loop stays compact in the instruction cache.
+template <typename Tin>
+__device__ __noinline__ uint4 load_straddle(const Tin* sl, const Tin* g, int e0, int len_bulk, int len) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    Tin xs[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+        const int ee = e0 + k;
+        Tin z = (Tin)(-INFINITY);
+        if (ee < len_bulk) z = sl[ee];
+        else if (ee < len) z = g[ee];
+        xs[k] = z;
+    }
+    return *reinterpret_cast<const uint4*>(xs);
+}
+
+// An item whose slice is not a whole number of bulk-copied vectors of length VSe (the last
+// slice of a row, or a row length that is not a multiple of 16 bytes): each thread rewrites
+// its own vectors of the ring stage -- -inf past the row, the straddling vector element-wise
+// from the ring and global memory -- so the pass-1 loads stay unconditional.  Out of line.
+template <typename Tin, int L, int NV>
+__device__ __noinline__ void repair_stage(Tin* stage, const LevelDesc& lv, int64_t b, int64_t i, int64_t base,
+                                          int tid, int len_bulk, int len, int vse) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    constexpr int ES = (int)sizeof(Tin);
+    for (int l = 0; l < L; ++l) {
+        Tin* sl = stage + (size_t)l * VS;
+        for (int jv = 0; jv < NV; ++jv) {
+            const int e0 = (jv * CTH + tid) * VEC;
+            if (e0 + VEC <= len_bulk || e0 >= vse) continue;
+            uint4 v;
+            if (e0 >= len) {
+                v = ES == 2 ? make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u)
+                            : make_uint4(0xFF800000u, 0xFF800000u, 0xFF800000u, 0xFF800000u);
+            } else {
+                v = load_straddle<Tin>(sl, reinterpret_cast<const Tin*>(lv.ptr[l]) + b * lv.bs[l] + i * lv.ld[l] + base,
+                                       e0, len_bulk, len);
+            }
+            *reinterpret_cast<uint4*>(sl + e0) = v;
+        }
+    }
+    // these generic-proxy writes precede the next bulk copy (async proxy) into the stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 template <typename Tin, int L, bool GREEDY>
@@ -137,12 +220,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NV = CET / VEC;           // 1 (bf16) or 2 (f32) vectors per thread and row
     constexpr int ES = (int)sizeof(Tin);
-    constexpr int NR = 256 / (CET * L);     // TMEM item slots (256 columns per pass-1 warp)
-    static_assert(NR <= NRMAX && NR >= 2, "TMEM slots");
+    constexpr int NT = core_tslots(L);                       // TMEM item slots
+    constexpr int NSS = core_sslots(L, ES, (int)sizeof(Ctl<L>)); // shared-memory item slots
+    constexpr int NR = NT + NSS;
+    static_assert(NR <= NRMAX && NT >= 2, "item slots");
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int S = core_stages(L, ES);
     Tin* ring = reinterpret_cast<Tin*>(smem);
     Ctl<L>& c = *reinterpret_cast<Ctl<L>*>(smem + align_up((size_t)S * L * VS * ES, 128));
+    // shared-memory exponential slots: [slot][row][k][pass-1 thread] (conflict-free)
+    float* xslot = reinterpret_cast<float*>(smem + align_up((size_t)S * L * VS * ES, 128) + align_up(sizeof(Ctl<L>), 128));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int C = p.C;
@@ -153,6 +240,12 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     const int grp = blockIdx.x / C, sfix = blockIdx.x % C;
     const int n_my = grp < kgrp && grp < p.U ? (p.U - grp + kgrp - 1) / kgrp : 0;
 
+    // the ring tail [VSe, VS) of every row is never written by the bulk copies: -inf once, so
+    // that clean items load whole vectors unconditionally
+    for (int e = tid; e < S * L * (VS - VSe); e += blockDim.x) {
+        const int row = e / (VS - VSe);
+        ring[(size_t)row * VS + VSe + (e - row * (VS - VSe))] = (Tin)(-INFINITY);
+    }
     if (warp == W_PROD) {
         if (lane == 0) {
             for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], NCW); }
@@ -175,7 +268,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     auto stamp = [&](int j, int k) {
-        if (p.trace) p.trace[((int64_t)(grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
+        if (p.trace && !(p.dbg & 64)) p.trace[((int64_t)(grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
     };
     // (no runtime integer division on the hot loops: it would issue on the busy MUFU pipe)
     auto item = [&](int j, int64_t& u, int& s, int64_t& b, int64_t& i) {
@@ -187,9 +280,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         i = uu - bb * (uint32_t)p.K;
     };
 
-    if (warp < NCW) {
+    const bool dbg_idle = p.dbg != 0 && warp >= NCW && (warp != W_PROD || (p.dbg & 32));
+    if (dbg_idle) {
+    } else if (warp < NCW) {
         // ================================================================ pass-1 warps
         const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
+#ifdef MSD_PHASE_PROF
+        long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
         for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             int s;
@@ -200,36 +298,27 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int64_t base = (int64_t)s * VSe;
             const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
             const int len_bulk = (len * ES) / 16 * 16 / ES;
-            mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
+#ifdef MSD_PHASE_PROF
+            long long ck0 = clock64();
+#endif
+            if (!(p.dbg & 32)) mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
+#ifdef MSD_PHASE_PROF
+            long long ck1 = clock64();
+#endif
             if (tid == 0) stamp(j, 1);
             uint4 raw[L][NV];
             float tmax[L];
+            // the last slice of a row (or an unaligned row length): patch the stage first
+            if (len_bulk != VSe) repair_stage<Tin, L, NV>(ring + (size_t)st * L * VS, p.lv, b, i, base, tid, len_bulk, len, VSe);
+            // every vector from the ring ([VSe, VS) holds -inf from the prologue)
 #pragma unroll
             for (int l = 0; l < L; ++l) {
                 const Tin* sl = ring + ((size_t)st * L + l) * VS;
 #pragma unroll
-                for (int jv = 0; jv < NV; ++jv) {
-                    const int e0 = (jv * CTH + tid) * VEC;
-                    if (e0 + VEC <= len_bulk) {
-                        raw[l][jv] = *reinterpret_cast<const uint4*>(sl + e0);
-                    } else if (e0 >= len) {   // past the end of this slice: all -inf
-                        if (ES == 2) raw[l][jv] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
-                        else raw[l][jv] = make_uint4(0xFF800000u, 0xFF800000u, 0xFF800000u, 0xFF800000u);
-                    } else {   // the vector straddling the end of the row: element-wise
-                        const Tin* g = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
-                                       i * p.lv.ld[l] + base;
-                        Tin xs[VEC];
+                for (int jv = 0; jv < NV; ++jv) raw[l][jv] = *reinterpret_cast<const uint4*>(sl + (jv * CTH + tid) * VEC);
+            }
 #pragma unroll
-                        for (int k = 0; k < VEC; ++k) {
-                            const int ee = e0 + k;
-                            Tin z = (Tin)(-INFINITY);
-                            if (ee < len_bulk) z = sl[ee];
-                            else if (ee < len) z = g[ee];
-                            xs[k] = z;
-                        }
-                        raw[l][jv] = *reinterpret_cast<const uint4*>(xs);
-                    }
-                }
+            for (int l = 0; l < L; ++l) {
                 float tm = -INFINITY;
                 if (ES == 2) {
                     uint32_t mx = 0xFF80FF80u;
@@ -253,62 +342,76 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 }
                 tmax[l] = tm;
             }
+            // the slice is in registers now: hand the ring stage back to the producer
+            __syncwarp();
+            if (lane == 0 && !(p.dbg & 32)) mbar_arrive(&c.empty[st]);
             // per-warp max of all rows, the shuffle chains interleaved
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) tmax[l] = fmaxf(tmax[l], __shfl_xor_sync(0xffffffffu, tmax[l], o));
             }
-            if (j >= NR) {   // slot q (TMEM and wmx) must have been released by the pass-2 warps
+#ifdef MSD_PHASE_PROF
+            long long ck2 = clock64();
+#endif
+            if (p.dbg & 8) continue;   // debug: TMA ring only
+            if (j >= NR && !p.dbg) {   // slot q (TMEM and wmx) must have been released by the pass-2 warps
                 mbar_wait(&c.tm_empty[q], (uint32_t)(((j / NR) - 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             }
             if (tid == 0) stamp(j, 2);
+#ifdef MSD_PHASE_PROF
+            long long ck3 = clock64();
+#endif
             if (lane == 0) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
             }
             float Sv[L], Kv[L];
             int am[L];
-            float xprev[CET];
+            float2 yprev[CET / 2];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                float x[CET];
+                // y = z - m_w exactly (bf16 / clamped inputs), e = 2^(y log2 e) on the MUFU; the
+                // rest in packed fp32 pairs (FADD2 / FMUL2 / FFMA2): sum e and the KL numerator
+                // sum e (y_l - y_{l-1}) = sum e ((z_l - z_{l-1}) - (m_l - m_{l-1}))
+                const float2 nm = make_float2(-tmax[l], -tmax[l]);
+                const float2 l2e = make_float2(LOG2E, LOG2E);
+                const float2 neg1 = make_float2(-1.f, -1.f);
+                float e[CET];
+                float2 s2 = make_float2(0.f, 0.f), k2 = make_float2(0.f, 0.f);
+                am[l] = 0x7fffffff;
 #pragma unroll
-                for (int jv = 0; jv < NV; ++jv) {
-                    const uint4 r = raw[l][jv];
-                    if (ES == 2) {
-                        x[jv * 8 + 0] = bf16lo(r.x); x[jv * 8 + 1] = bf16hi(r.x);
-                        x[jv * 8 + 2] = bf16lo(r.y); x[jv * 8 + 3] = bf16hi(r.y);
-                        x[jv * 8 + 4] = bf16lo(r.z); x[jv * 8 + 5] = bf16hi(r.z);
-                        x[jv * 8 + 6] = bf16lo(r.w); x[jv * 8 + 7] = bf16hi(r.w);
-                    } else {
-                        x[(jv * 4 + 0) % CET] = __uint_as_float(r.x); x[(jv * 4 + 1) % CET] = __uint_as_float(r.y);
-                        x[(jv * 4 + 2) % CET] = __uint_as_float(r.z); x[(jv * 4 + 3) % CET] = __uint_as_float(r.w);
+                for (int pp = 0; pp < CET / 2; ++pp) {
+                    const float2 xv = elem_pair<Tin>(raw[l][(2 * pp) / VEC], pp % (VEC / 2));
+                    const float2 y = __fadd2_rn(xv, nm);
+                    const float2 t = __fmul2_rn(y, l2e);
+                    const float2 ev = make_float2(ex2f(t.x), ex2f(t.y));
+                    e[2 * pp] = ev.x;
+                    e[2 * pp + 1] = ev.y;
+                    s2 = __fadd2_rn(s2, ev);
+                    if (l > 0) k2 = __ffma2_rn(ev, __ffma2_rn(yprev[pp], neg1, y), k2);
+                    yprev[pp] = y;
+                    if (GREEDY) {
+                        const int k0 = 2 * pp;
+                        const int i0 = (int)(base + ((k0 / VEC) * CTH + tid) * VEC + (k0 % VEC));
+                        if (xv.x == tmax[l]) am[l] = min(am[l], i0);
+                        if (xv.y == tmax[l]) am[l] = min(am[l], i0 + 1);
                     }
                 }
-                const float m = tmax[l];
-                const float shift = l > 0 ? m - tmax[l > 0 ? l - 1 : 0] : 0.f;
-                float e[CET];
-                float sum = 0.f, ks = 0.f;
+                if (q < NT) {
+                    tm_st16(tbase + (uint32_t)(q * CET * L + l * CET), e);
+                } else {
+                    float* xs = xslot + ((size_t)((q - NT) * L + l) * CET) * CTH + tid;
 #pragma unroll
-                for (int k = 0; k < CET; ++k) {
-                    e[k] = ex2f((x[k] - m) * LOG2E);
-                    sum += e[k];
-                    if (l > 0) ks = fmaf(e[k], (x[k] - xprev[k]) - shift, ks);
+                    for (int k = 0; k < CET; ++k) xs[k * CTH] = e[k];
                 }
-                tm_st16(tbase + (uint32_t)(q * CET * L + l * CET), e);
-                Sv[l] = sum;
-                Kv[l] = ks;
-                am[l] = 0x7fffffff;
-                if (GREEDY) {
-#pragma unroll
-                    for (int k = CET - 1; k >= 0; --k)
-                        if (x[k] == m) am[l] = (int)(base + ((k / VEC) * CTH + tid) * VEC + (k % VEC));
-                }
-#pragma unroll
-                for (int k = 0; k < CET; ++k) xprev[k] = x[k];
+                Sv[l] = s2.x + s2.y;
+                Kv[l] = k2.x + k2.y;
             }
+#ifdef MSD_PHASE_PROF
+            long long ck4 = clock64();
+#endif
 #pragma unroll
             for (int l = 0; l < L; ++l) {
                 Sv[l] = fold4(Sv[l]);
@@ -318,7 +421,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) am[l] = warp_min_i(am[l]);
             }
-            if (j >= R1) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
+#ifdef MSD_PHASE_PROF
+            long long ck5 = clock64();
+#endif
+            if (j >= R1 && !p.dbg) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
             if (lane < NSUB) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
@@ -330,16 +436,31 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     for (int l = 0; l < L; ++l) c.r1A[r1][l][warp] = am[l];
                 }
             }
+#ifdef MSD_PHASE_PROF
+            long long ck6 = clock64();
+#endif
             tm_wait_st();
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (tid == 0) stamp(j, 3);
+#ifdef MSD_PHASE_PROF
+            if (p.dbg & 64) {   // debug: pass-1 phase cycle profile (register accumulators)
+                long long ck7 = clock64();
+                pc[0] += ck1 - ck0; pc[1] += ck2 - ck1; pc[2] += ck3 - ck2; pc[3] += ck4 - ck3;
+                pc[4] += ck5 - ck4; pc[5] += ck6 - ck5; pc[6] += ck7 - ck6; pc[7] += 1;
+            }
+#endif
             if (lane == 0) {
-                mbar_arrive(&c.empty[st]);
-                mbar_arrive(&c.r1_full[r1]);
-                mbar_arrive(&c.tm_full[q]);
+                if (!p.dbg) {
+                    mbar_arrive(&c.r1_full[r1]);
+                    mbar_arrive(&c.tm_full[q]);
+                }
             }
         }
+#ifdef MSD_PHASE_PROF
+        if ((p.dbg & 64) && p.trace && lane == 0)
+            for (int k = 0; k < 8; ++k) atomicAdd(p.trace + warp * 8 + k, (unsigned long long)pc[k]);
+#endif
     } else if (warp < W_PROD) {
         // ================================================================ pass-2 warps
         // warp NCW + w reads the TMEM lanes / columns written by pass-1 warp w
@@ -362,9 +483,18 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             if (w == 0 && lane == 0) stamp(j, 12);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             float ev[L][CET];
+            if (q < NT) {
 #pragma unroll
-            for (int l = 0; l < L; ++l) tm_ld16(tbase + (uint32_t)(q * CET * L + l * CET), ev[l]);
-            tm_wait_ld();
+                for (int l = 0; l < L; ++l) tm_ld16(tbase + (uint32_t)(q * CET * L + l * CET), ev[l]);
+                tm_wait_ld();
+            } else {
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    const float* xs = xslot + ((size_t)((q - NT) * L + l) * CET) * CTH + w * 32 + lane;
+#pragma unroll
+                    for (int k = 0; k < CET; ++k) ev[l][k] = xs[k * CTH];
+                }
+            }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.tm_empty[q]);
@@ -497,7 +627,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
         // ================================================================ fetchers (pass-2 factors)
         const int f = warp - W_FETCH0;
-        const int LC = L * C;
+        const int LC = L * C;     // <= FBUF (checked on the host)
         unsigned long long* fb = c.fbuf[f];
         for (int j = f; j < n_my; j += NFETCH) {
             int64_t u, b, i;
@@ -511,7 +641,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
             while (true) {
                 // all loads in flight before any use (one round trip), then stage in smem
-                constexpr int MAXB = (MAXL * 128 + 31) / 32;
+                constexpr int MAXB = FBUF / 32;
                 unsigned long long rr[MAXB];
 #pragma unroll
                 for (int t = 0; t < MAXB; ++t) {
@@ -585,7 +715,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp2f_fma((wb - Mb) * LOG2E) : 0.f;
                     const bool skip = !(ca > 0.f) || !(Sa > 0.f) || !(Sb > 0.f) || !isfinite(Sa) || !isfinite(Sb);
                     WF wf;
-                    wf.rho = skip ? 0.f : (cb * Sa) * frcp_fma(Sb * ca);
+                    // identical rows must give rho = 1 exactly (zero residual), which the
+                    // Newton reciprocal alone does not guarantee
+                    const float num = cb * Sa, den = Sb * ca;
+                    wf.rho = skip ? 0.f : (num == den ? 1.f : num * frcp_fma(den));
                     wf.scale = skip ? 0.f : ca * frcp_fma(Sa);
                     c.rowf[q][l][w] = wf;
                 }
@@ -640,7 +773,9 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     const size_t stage_bytes = (size_t)L * VS * ES;
     const int S = core_stages(L, ES);
     p.stages = S;
-    const size_t smem = align_up(stage_bytes * S, 128) + sizeof(Ctl<L>) + 128;
+    const int nss = core_sslots(L, ES, (int)sizeof(Ctl<L>));
+    const size_t smem = align_up(stage_bytes * S, 128) + align_up(sizeof(Ctl<L>), 128) +
+                        (size_t)nss * L * CET * CTH * 4 + 128;
     auto k = core_kernel<Tin, L, G>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -650,6 +785,7 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, CORE_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
+    if (L * p.C > FBUF) return cudaErrorInvalidValue;   // vocabulary too large for the exchange buffer
     // one CTA per SM (it owns all 512 TMEM columns); k = floor(nsm / C) groups of C CTAs
     int64_t kg = nsm / p.C;
     if (kg < 1) return cudaErrorInvalidConfiguration;

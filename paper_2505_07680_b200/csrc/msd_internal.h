@@ -35,7 +35,8 @@ struct CoreParams {
     uint32_t* ready;
     uint32_t* flags;
     uint32_t* err;
-    unsigned long long* trace;   // debug: 8 globaltimer stamps per item, or NULL
+    unsigned long long* trace;   // debug: 16 globaltimer stamps per item, or NULL
+    int32_t dbg;                 // debug isolation mode (MSD_CORE_DBG): 0 = normal
 };
 
 struct TailParams {

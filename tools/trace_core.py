@@ -51,3 +51,9 @@ for g in (0, 100):
 # who is last in each unit: distribution of CTA index of the last publisher
 lastc = np.nanargmax(pub, 1)
 print("C", C, "groups", kg)
+# per-CTA start / end (first TMA issue, last stamp of any kind)
+first = np.array([np.nanmin(t[cta == g, 0]) for g in range(G)])
+lastx = np.array([np.nanmax(t[cta == g]) for g in range(G)])
+print("CTA first-issue us: min %.1f med %.1f max %.1f" % (first.min(), np.median(first), first.max()))
+print("CTA last-stamp  us: min %.1f med %.1f max %.1f" % (lastx.min(), np.median(lastx), lastx.max()))
+print("slowest CTAs:", np.argsort(-lastx)[:8].tolist(), "earliest-finishing:", np.argsort(lastx)[:8].tolist())
