@@ -150,6 +150,10 @@ msd_status run_engine(const Engine& E) {
     cp.err = reinterpret_cast<uint32_t*>(ws + w.hdr);
     cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
     cp.dbg = (int32_t)env_double("MSD_CORE_DBG", 0.0);
+    {
+        cudaError_t pe = core_pad(&cp.pad);
+        if (pe != cudaSuccess) return cuda_fail(pe, "pad buffer");
+    }
 
     TailParams tp;
     memset(&tp, 0, sizeof(tp));

@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             if (tid == 0) stamp(j, 1);
             uint4 raw[L][NV];
             float tmax[L];
-            // the last slice of a row (or an unaligned row length): patch the stage first
-            if (len_bulk != VSe) repair_stage<Tin, L, NV>(ring + (size_t)st * L * VS, p.lv, b, i, base, tid, len_bulk, len, VSe);
+            // a row length that is not a multiple of 16 bytes: patch the straddling vector
+            if (len_bulk != len) repair_stage<Tin, L, NV>(ring + (size_t)st * L * VS, p.lv, b, i, base, tid, len_bulk, len, VSe);
             // every vector from the ring ([VSe, VS) holds -inf from the prologue)
 #pragma unroll
             for (int l = 0; l < L; ++l) {
@@ -535,15 +535,20 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 item(j, u, s, b, i);
                 const int64_t len = max((int64_t)0, min((int64_t)VSe, p.V - (int64_t)s * VSe));
                 const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
+                // the last slice of a row: pad [bulk end, VSe) from the constant pad buffer so
+                // the pass-1 loads stay unconditional (the copy engine does the fill)
+                const uint32_t pad = (uint32_t)(VSe * ES) - bytes;
                 stamp(j, 0);
-                mbar_arrive_expect_tx(&c.full[st], bytes * L);
-                if (bytes) {
+                mbar_arrive_expect_tx(&c.full[st], (bytes + pad) * L);
 #pragma unroll
-                    for (int l = 0; l < L; ++l) {
+                for (int l = 0; l < L; ++l) {
+                    Tin* dst = ring + ((size_t)st * L + l) * VS;
+                    if (bytes) {
                         const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
                                          i * p.lv.ld[l] + (int64_t)s * VSe;
-                        bulk_g2s(ring + ((size_t)st * L + l) * VS, src, bytes, &c.full[st], pol);
+                        bulk_g2s(dst, src, bytes, &c.full[st], pol);
                     }
+                    if (pad) bulk_g2s(reinterpret_cast<unsigned char*>(dst) + bytes, p.pad, pad, &c.full[st], pol);
                 }
             }
         }
@@ -793,6 +798,29 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     const int64_t grid = kg * p.C;
     void* args[] = {&p};
     return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(CORE_THREADS), args, smem, s);
+}
+
+// 0xF1 bytes: bf16 0xF1F1 and f32 0xF1F1F1F1 are both ~ -2.4e30, i.e. masked (-inf after the
+// -1e30 clamp) -- the fill of a row's last slice beyond the vocabulary
+__device__ __align__(128) unsigned char g_pad[VS * 4];
+
+cudaError_t core_pad(const void** out) {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    void* ptr = nullptr;
+    e = cudaGetSymbolAddress(&ptr, g_pad);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+        e = cudaMemset(ptr, 0xF1, sizeof(g_pad));
+        if (e != cudaSuccess) return e;
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return e;
+        done[dev] = true;
+    }
+    *out = ptr;
+    return cudaSuccess;
 }
 
 cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s) {

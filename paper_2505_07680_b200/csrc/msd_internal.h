@@ -37,7 +37,11 @@ struct CoreParams {
     uint32_t* err;
     unsigned long long* trace;   // debug: 16 globaltimer stamps per item, or NULL
     int32_t dbg;                 // debug isolation mode (MSD_CORE_DBG): 0 = normal
+    const void* pad;             // >= VS * 4 bytes of 0xF1 (bf16 / f32 ~ -2.4e30, below the -1e30 clamp)
 };
+
+// the constant pad buffer of the current device (filled on first use)
+cudaError_t core_pad(const void** out);
 
 struct TailParams {
     LevelDesc lv;
