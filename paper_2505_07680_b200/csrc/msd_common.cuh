@@ -45,8 +45,8 @@ struct RowStat {
 };
 
 // Slice geometry of a vocabulary of V entries: C slices of VSe (<= VS) entries.  C is
-// the smallest value in [ceil(V/VS), 2 ceil(V/VS)] for which k = floor(148/C) groups of C
-// CTAs keep >= 144 SMs busy (a group owns whole units, so units never straddle rounds and
+// the smallest value in [ceil(V/VS), 5/4 ceil(V/VS)] for which k = floor(148/C) groups of C
+// CTAs keep the most SMs busy (a group owns whole units, so units never straddle rounds and
 // the groups never wait on each other; see msd_core.cu).
 struct SliceGeom {
     int32_t C;
@@ -55,9 +55,11 @@ struct SliceGeom {
 constexpr int REF_SMS = 148;   // B200
 __host__ __device__ inline SliceGeom slice_geometry(int64_t V) {
     const int32_t cmin = (int32_t)((V + VS - 1) / VS);
+    // the smallest C in [cmin, 5 cmin / 4] (slices stay >= 80% of VS) that keeps the most SMs
+    // busy (all 148 if possible): k = floor(148 / C) groups of C CTAs
     int32_t best = cmin, used = (REF_SMS / cmin) * cmin;
-    for (int32_t c = cmin + 1; c <= 2 * cmin && c <= REF_SMS && used < REF_SMS - 4; ++c) {
-        const int32_t u = (REF_SMS / c) * c;   // smallest C that keeps >= 144 of 148 SMs busy
+    for (int32_t c = cmin + 1; c <= cmin + cmin / 4 && c <= REF_SMS && used < REF_SMS; ++c) {
+        const int32_t u = (REF_SMS / c) * c;
         if (u > used) { used = u; best = c; }
     }
     SliceGeom g;

@@ -11,7 +11,7 @@ cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"])
 lib = api.lib(); lib.msd_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 def geo(V, VS=4096, REF=148):
     cmin = (V + VS - 1) // VS; best = cmin; used = (REF // cmin) * cmin; cc = cmin + 1
-    while cc <= 2 * cmin and cc <= REF and used < REF - 4:
+    while cc <= cmin + cmin // 4 and cc <= REF and used < REF:
         u = (REF // cc) * cc
         if u > used: used = u; best = cc
         cc += 1
