@@ -40,13 +40,9 @@ def _peaks():
         return {}
 
 
-def _dist():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws > 1 and not torch.distributed.is_initialized():
-        torch.distributed.init_process_group("nccl")
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+def _dist(backend="nccl"):
+    from paper_2505_07680_b200 import dist as mdist
+    return mdist.init_from_env(backend)
 
 
 class ClockSampler:
@@ -135,7 +131,7 @@ def host_cores():
 
 
 def run_reference(args):
-    ws, rank, local = _dist()
+    ws, rank, local = _dist("gloo")
     if rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
@@ -167,13 +163,13 @@ def run_reference(args):
 
 def run_ours(args):
     from paper_2505_07680_b200 import api
+    from paper_2505_07680_b200 import dist as mdist
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = synth.CONFIGS[args.config]
-    B = cfg["B"] if args.scaling == "weak" else cfg["B"] // ws
-    req0 = rank * B
+    req0, B = mdist.shard(cfg["B"], ws, rank, args.scaling)
     c, inp, kv = build_workload(args.config, B, req0, dev)
     L, K, V = c["L"], c["K"], c["V"]
     esize = 2 if c["dtype"] == "bf16" else 4
@@ -189,33 +185,23 @@ def run_ours(args):
 
     pinned_stats = [torch.zeros_like(cv.stats, device="cpu").pin_memory() for _ in range(3)]
     stat_ev = [torch.cuda.Event() for _ in range(3)]
-    sched = {"sim": [0.5] * (L - 1), "first": True, "chain": list(range(L)), "steps": 0}
     T_ms = [1.0, 3.0, 10.0, 40.0][-L:]   # synthetic per-token times (invented)
+    sched = mdist.ChainScheduler(T_ms=T_ms, W=K)
 
     def host_scheduler(j):
-        # consume the stats of step j-2 (already complete): EMA SimScore -> Alg. 1
+        # consume the (all-reduced) stats of step j-2, complete by now: EMA SimScore -> Alg. 1
         if j < 2:
             return
         slot = (j - 2) % 3
         stat_ev[slot].synchronize()
-        rows = pinned_stats[slot].tolist()
-        for l in range(L - 1):
-            sched["sim"][l] = api.simscore_update(sched["sim"][l], rows[l], 0.1, sched["first"])
-        sched["first"] = False
-        P = L
-        sim = [[0.0] * P for _ in range(P)]
-        for l in range(L - 1):
-            sim[l][l + 1] = sched["sim"][l]
-        sched["chain"], sched["t_eff"] = api.select_chain(T_ms, sim, K, max_len=L)
-        sched["steps"] += 1
+        sched.update(pinned_stats[slot].tolist())
 
     def step(j):
         reset_kv()
         cv.stats.zero_()
         cv()
         rb()
-        if ws > 1:
-            torch.distributed.all_reduce(cv.stats)
+        mdist.allreduce_stats(cv.stats)
         slot = j % 3
         pinned_stats[slot].copy_(cv.stats, non_blocking=True)
         stat_ev[slot].record()
@@ -289,8 +275,7 @@ def run_ours(args):
             cv.stats.zero_()
             cv()
             rb()
-            if ws > 1:
-                torch.distributed.all_reduce(cv.stats)
+            mdist.allreduce_stats(cv.stats)
             h_out["commit_tok"].copy_(cv.commit_tok, non_blocking=True)
             h_out["commit_len"].copy_(cv.commit_len, non_blocking=True)
             h_out["stats"].copy_(cv.stats, non_blocking=True)
@@ -343,8 +328,7 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
-            "scheduler": {"chain": sched.get("chain"), "simscore": sched["sim"],
-                          "t_eff_ms": sched.get("t_eff")},
+            "scheduler": {"chain": sched.chain, "simscore": sched.sim, "t_eff_ms": sched.t_eff},
             "timeouts": n_timeout,
         }
         print(json.dumps(line), flush=True)
