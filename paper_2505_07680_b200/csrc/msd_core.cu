@@ -5,44 +5,71 @@
 // exactly once.
 //
 // Decomposition.  A *unit* is one (request b, draft position i < K) and owns the L
-// rows Z_l[b, i, :].  A unit is cut into C slices of VS = 4096 vocabulary entries;
-// an *item* is (unit, slice).  The kernel is persistent and cooperative (one CTA per
-// SM): CTA g processes items g, g+G, g+2G, ...; the C items of a unit run on C CTAs,
-// which exchange per-slice (max, sum) records through global memory.
+// rows Z_l[b, i, :].  A unit is cut into C slices of VSe <= VS = 4096 vocabulary
+// entries; an *item* is (unit, slice).  The kernel is persistent and cooperative (one
+// CTA per SM) and runs k = floor(148 / C) groups of C CTAs: CTA (g, s) processes slice s
+// of units g, g + k, ..., so the C items of a unit run concurrently on C SMs, which
+// exchange per-slice (max, sum) records through global memory.
 //
-// Warp specialisation (16 compute + 7 service warps):
-//   compute  pass 1 of item j: per-warp max of each row (the only cross-lane step),
-//            e_v = 2^((z_v - m_w) log2 e) -- one MUFU.EX2 per element --, per-thread sums
-//            (S, KL numerator) to shared memory, e_v parked in TMEM (tcgen05.st);
-//            then pass 2 of item j-LAG: e_v back from TMEM (tcgen05.ld), per-thread residual
-//            sum_v max(p_v - q_v, 0) of every adjacent pair to shared memory.
-//   producer TMA bulk copies (cp.async.bulk) of the L row slices into an S-stage ring.
-//   publisher folds pass-1 records into the slice record (float64 combine), publishes a
-//            self-validating 64-bit (max, sum) record per row with a relaxed store and bumps
-//            the unit counter with a relaxed red (no fence on the critical path).
-//   fetchers (4, items j = f mod 4) poll the unit counter, load the unit's C records in one
-//            round trip (re-loading if one is not yet visible), combine them (float64) into
-//            the row normalisers and derive the per-warp pass-2 factors of this slice.
-//   reducer  folds pass-2 records into the slice residual R_s (float64).
-// The exchange latency hides behind LAG items of pass 1: TMEM holds LAG+1 items of
-// exponentials per compute thread (128 columns / (8 L)).
+// Two passes per item; pass 2 needs the row normalisers, i.e. the records of all C
+// slices, so an item stays on chip from its arrival until the exchange completes
+// (several microseconds under full HBM load).  Two kinds of item keep it on chip:
+//   T items  pass 1 parks the exponentials e in TMEM (fp32) and releases the ring stage at
+//            once; pass 2 reads e back (tcgen05.ld) -- no recomputation.
+//   R items  pass 1 keeps the ring stage (bf16, half the bytes of e); pass 2 recomputes e
+//            from it (one more MUFU.EX2 per element) and releases the stage.
+// Of every pat_p items the first pat_t are T items (host-chosen).
+//
+// Exponent reference.  e = 2^((z - R) log2 e) needs no maximum: any R works while no
+// z - R exceeds ~88 (fp32 range).  The fast path takes R_l = the slice's first logit of row
+// l, read by every thread with one broadcast load, so all warps of the slice share it: no
+// max tree, no cross-lane max, and the per-warp factors of the exchange are all 1.  A
+// non-finite result (overflow, -inf or NaN inputs, a masked first entry) sends the warp to
+// the clamped slow path, whose reference is the warp maximum (records carry their warp's
+// reference, so the two mix freely).  Greedy mode (argmax needed) always takes the max path.
+//
+// Warp roles (7 service + 4 pass-2 + 8 pass-1 warps; low warp ids first):
+//   producer  TMA bulk copies (cp.async.bulk) of the L row slices into the S-stage ring.
+//   publisher folds the pass-1 warp records into the slice record and publishes it.
+//   fetchers  (items j = f mod NFETCH) poll the unit's L x C records, combine them into the
+//             row normalisers relative to this slice's references, and derive the pass-2
+//             factors.
+//   reducer   folds the pass-2 records into the slice residual R_s (probability units).
+//   pass 2    per-region residual sum max(e_l - rho e_{l-1}, 0) of every adjacent pair --
+//             this slice's share of DTV (Eq. 5) and of the residual CDF.
+//   pass 1    warp w owns the contiguous 512-entry region [512 w, 512 w + 512) of the slice
+//             (warps past the slice end idle): y = z - R with the mixed-precision
+//             add.f32.bf16 (no unpacking), e = 2^(y log2 e) on the MUFU, the sum of e and the
+//             KL numerator sum e_l (y_l - y_{l-1}) in packed fp32.
 #include "msd_common.cuh"
 #include "msd_internal.h"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace msd {
 
-constexpr int NCW = 8;                 // pass-1 warps (pass-2 warps: NCW .. 2 NCW - 1)
+constexpr int NCW = 8;                 // pass-1 warps = element regions of a slice
+constexpr int NCW2 = 4;                // pass-2 warps: warp v handles regions v and v + 4
 constexpr int CTH = NCW * 32;          // pass-1 threads
 constexpr int CET = VS / CTH;          // elements per pass-1 thread per row (16)
-constexpr int NFETCH = 5;
-constexpr int W_P2 = NCW, W_PROD = 2 * NCW, W_PUB = 2 * NCW + 1, W_FETCH0 = 2 * NCW + 2,
-              W_RED = W_FETCH0 + NFETCH;
-constexpr int CORE_THREADS = (W_RED + 1) * 32;
-constexpr int SMAX = 6;
+constexpr int WCH = CET * 32;          // contiguous slice entries per pass-1 warp (512)
+constexpr int TCOLS = 256;             // TMEM columns per region (2 regions per lane quadrant)
+constexpr int NFETCH = 4;
+// Warp numbering: latency-critical service warps first, then pass 2, then the throughput
+// warps (pass 1).  Pass-1 warp W_P1 + r owns region r in TMEM lane quadrant r % 4; pass-2
+// warp W_P2 + v serves regions v and v + 4 (quadrant v): both bases are multiples of 4.
+constexpr int W_PROD = 0, W_PUB = 1, W_FETCH0 = 2, W_RED = W_FETCH0 + NFETCH;
+constexpr int W_P2 = 8, W_P1 = W_P2 + NCW2;
+constexpr int NG1 = 2;                 // pass-1 warp groups: group g processes items j = g mod NG1
+constexpr int CORE_THREADS = (W_P1 + NG1 * NCW) * 32;
+static_assert(W_RED < W_P2 && W_P2 % 4 == 0 && W_P1 % 4 == 0 && NCW == 2 * NCW2, "warp roles");
+constexpr int SMAX = 14;               // ring stages (upper bound)
+constexpr int NQ = 16;                 // per-item record slots (references, pass-2 factors)
+constexpr int NTMAX = 8;               // TMEM item slots (upper bound)
 constexpr int FBUF = 192;              // records per fetcher staging buffer (L * C <= 192)
 constexpr int SMEM_BUDGET = 227 * 1024;
-constexpr int NRMAX = 8;
-constexpr int R1 = 3, R2 = 3;          // pass-1 / pass-2 record rings
+constexpr int R1 = 4, R2 = 4;          // pass-1 / pass-2 record rings (powers of two)
 constexpr int NSUB = 4;                // per-warp records after a 3-step shuffle fold (lanes 0..3)
 static_assert(CET == 16, "two 16-byte bf16 vectors per thread and row");
 
@@ -54,34 +81,23 @@ template <int L>
 struct Ctl {
     uint64_t full[SMAX], empty[SMAX];
     uint64_t r1_full[R1], r1_empty[R1], r2_full[R2], r2_empty[R2];
-    uint64_t rowf_full[NRMAX], rowf_empty[NRMAX];
-    uint64_t tm_full[NRMAX], tm_empty[NRMAX];   // TMEM item slots: pass-1 warps -> pass-2 warps
+    uint64_t rowf_full[NQ], rowf_empty[NQ];
+    uint64_t tm_full[NTMAX], tm_empty[NTMAX];  // TMEM item slots: pass-1 warps -> pass-2 warps
+    uint64_t pub[NQ];                       // this CTA's slice record of item j is published
     uint32_t taddr;
-    float wmx[NRMAX][L][NCW];               // per-warp max of each row, per item slot
+    float wmx[NQ][L][NCW];                  // per-warp max of each row, per item
+    uint32_t clampw[NQ];                    // bit w: pass-1 warp w took the clamped path
     float r1S[R1][L][NCW][NSUB];            // pass-1 partial sums
     float r1K[R1][L][NCW][NSUB];            // pass-1 KL numerators (relative to the warp shift)
     int r1A[R1][L][NCW];                    // greedy: first argmax index per warp
-    WF rowf[NRMAX][L][NCW];
-    float r2R[R2][L][NCW][NSUB];            // pass-2 residual partials
-    float r2scale[R2][L][NCW];
-    unsigned long long fbuf[NFETCH][FBUF];       // fetcher staging of a unit's records
+    WF rowf[NQ][L][NCW];
+    float r2R[R2][L][NCW2][NSUB];           // pass-2 residual partials (probability units)
+    unsigned long long fbuf_pad;
+    unsigned long long fbuf[NFETCH][FBUF];  // fetcher staging of a unit's records
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void red_add_release(uint32_t* p, uint32_t v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-    uint32_t r;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
-    return r;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-    unsigned long long r;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
-    return r;
 }
 // relaxed load without a compiler memory clobber: independent loads stay in flight together
 __device__ __forceinline__ unsigned long long ld_relaxed_u64_nc(const unsigned long long* p) {
@@ -92,35 +108,63 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64_nc(const unsigned l
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// TMEM stores / loads of 8 consecutive columns (no "memory" clobber: TMEM is ordered by the
+// tcgen05.wait / fence instructions, and arithmetic may be scheduled across these)
 __device__ __forceinline__ void tm_st16(uint32_t ta, const float* v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
         "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
-        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
-        : "memory");
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]));
 }
 __device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
           "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
-        : "r"(ta)
+        : "r"(ta));
+}
+// non-blocking probe of a phase (no suspend)
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return done != 0;
 }
-__device__ __forceinline__ void tm_st8(uint32_t ta, const float* v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
-                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
-                 : "memory");
-}
-__device__ __forceinline__ void tm_ld8(uint32_t ta, float* v) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
-                 : "r"(ta)
-                 : "memory");
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint32_t clamp_bf16x2(uint32_t w) { return max_nan_bf16x2(w, 0xF149F149u); }
+
+// warp max (NaN-propagating) in one instruction (CREDUX)
+__device__ __forceinline__ float redux_max_nan(float v) {
+    float r;
+    asm("redux.sync.max.NaN.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ int redux_min_s32(int v) {
+    int r;
+    asm("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+// bf16 half of a packed word plus an fp32 value, in fp32 (FHADD.BF16: no unpacking)
+__device__ __forceinline__ float bf16lo_add(uint32_t w, float c) {
+    float r;
+    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %1; add.rn.f32.bf16 %0, lo, %2; }" : "=f"(r) : "r"(w), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float bf16hi_add(uint32_t w, float c) {
+    float r;
+    asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %1; add.rn.f32.bf16 %0, hi, %2; }" : "=f"(r) : "r"(w), "f"(c));
+    return r;
+}
+__device__ __forceinline__ uint32_t word_of(const uint4& r, int k) {
+    return k == 0 ? r.x : k == 1 ? r.y : k == 2 ? r.z : r.w;
+}
 
 // fold a per-lane value into lanes 0..3 (lane k holds the sum over lanes == k mod 4)
 __device__ __forceinline__ float fold4(float v) {
@@ -130,55 +174,35 @@ __device__ __forceinline__ float fold4(float v) {
     return v;
 }
 
-// TMA ring depth: 4 stages of 24-32 KB (bf16, L = 3-4) keep ~2 us of HBM data in flight.
-#ifndef MSD_RING_BYTES
-#define MSD_RING_BYTES 98304
-#endif
-__host__ __device__ constexpr int core_stages(int L, int es) {
-    return (MSD_RING_BYTES / (L * VS * es)) < 2 ? 2
-         : ((MSD_RING_BYTES / (L * VS * es)) > SMAX ? SMAX : (MSD_RING_BYTES / (L * VS * es)));
-}
-// item slots of parked exponentials: TMEM holds 256 / (16 L) items per pass-1 warp; the
-// shared memory left after the ring and the control block adds 1-2 more (L = 3, 4).
-__host__ __device__ constexpr int core_tslots(int L) { return 256 / (CET * L); }
-__host__ __device__ constexpr int core_sslots_raw(int L, int es, int ctl_bytes) {
-    return (SMEM_BUDGET - core_stages(L, es) * L * VS * es - ctl_bytes - 1024) / (L * CET * CTH * 4);
-}
-#ifndef MSD_SSLOTS_MAX
-#define MSD_SSLOTS_MAX 0   // measured: parking items in shared memory costs more than it hides
-#endif
-__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
-__host__ __device__ constexpr int core_sslots(int L, int es, int ctl_bytes) {
-    return core_sslots_raw(L, es, ctl_bytes) < 0
-               ? 0
-               : cmin(cmin(core_sslots_raw(L, es, ctl_bytes), MSD_SSLOTS_MAX), NRMAX - core_tslots(L));
+// 2^x in float32 on the FMA/ALU pipes (no MUFU: its queue is full of pass-1 ex2); +inf
+// above 2^127, 0 below 2^-126.
+__device__ __forceinline__ float exp2f_fma_any(float x) {
+    if (x > 127.f) return INFINITY;
+    return exp2f_fma(x);
 }
 
-// elements (2 pp, 2 pp + 1) of a thread's 16-byte vector as a float pair
+__host__ __device__ constexpr int core_tslots(int L) { return TCOLS / (CET * L); }
+
+// element index (within the slice) of vector jv of pass-1 thread (warp w, lane)
 template <typename Tin>
-__device__ __forceinline__ float2 elem_pair(const uint4& r, int pp);
-template <>
-__device__ __forceinline__ float2 elem_pair<__nv_bfloat16>(const uint4& r, int pp) {
-    const uint32_t w = pp == 0 ? r.x : pp == 1 ? r.y : pp == 2 ? r.z : r.w;
-    return make_float2(bf16lo(w), bf16hi(w));
-}
-template <>
-__device__ __forceinline__ float2 elem_pair<float>(const uint4& r, int pp) {
-    return pp == 0 ? make_float2(__uint_as_float(r.x), __uint_as_float(r.y))
-                   : make_float2(__uint_as_float(r.z), __uint_as_float(r.w));
+__device__ __forceinline__ int vec_index(int w, int lane, int jv) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    constexpr int NV = CET / VEC;
+    return (w * NV + jv) * 32 * VEC + lane * VEC;
 }
 
 // The VEC-element vector that straddles the end of a row: the bulk-copied part from shared
-// memory, the tail (< 16 bytes) from global memory, -inf past the row.  Out of line so the
-// pass-1 loop stays compact in the instruction cache.
+// memory, the tail (< 16 bytes) from global memory, the pad value (~ -2.4e30) past the row.
 template <typename Tin>
 __device__ __noinline__ uint4 load_straddle(const Tin* sl, const Tin* g, int e0, int len_bulk, int len) {
     constexpr int VEC = Elem<Tin>::VEC;
+    uint4 pv = make_uint4(0xF1F1F1F1u, 0xF1F1F1F1u, 0xF1F1F1F1u, 0xF1F1F1F1u);
     Tin xs[VEC];
+    const Tin* pz = reinterpret_cast<const Tin*>(&pv);
 #pragma unroll
     for (int k = 0; k < VEC; ++k) {
         const int ee = e0 + k;
-        Tin z = (Tin)(-INFINITY);
+        Tin z = pz[k];
         if (ee < len_bulk) z = sl[ee];
         else if (ee < len) z = g[ee];
         xs[k] = z;
@@ -186,28 +210,20 @@ __device__ __noinline__ uint4 load_straddle(const Tin* sl, const Tin* g, int e0,
     return *reinterpret_cast<const uint4*>(xs);
 }
 
-// An item whose slice is not a whole number of bulk-copied vectors of length VSe (the last
-// slice of a row, or a row length that is not a multiple of 16 bytes): each thread rewrites
-// its own vectors of the ring stage -- -inf past the row, the straddling vector element-wise
-// from the ring and global memory -- so the pass-1 loads stay unconditional.  Out of line.
+// An item whose row length is not a whole number of 16-byte vectors: each pass-1 thread
+// rewrites its own straddling vector of the ring stage from the ring and global memory, so
+// the pass-1 loads stay unconditional.  Out of line.
 template <typename Tin, int L, int NV>
-__device__ __noinline__ void repair_stage(Tin* stage, const LevelDesc& lv, int64_t b, int64_t i, int64_t base,
-                                          int tid, int len_bulk, int len, int vse) {
+__device__ __noinline__ void repair_stage(Tin* stage, int rs, const LevelDesc& lv, int64_t b, int64_t i,
+                                          int64_t base, int w, int lane, int len_bulk, int len) {
     constexpr int VEC = Elem<Tin>::VEC;
-    constexpr int ES = (int)sizeof(Tin);
     for (int l = 0; l < L; ++l) {
-        Tin* sl = stage + (size_t)l * VS;
+        Tin* sl = stage + (size_t)l * rs;
         for (int jv = 0; jv < NV; ++jv) {
-            const int e0 = (jv * CTH + tid) * VEC;
-            if (e0 + VEC <= len_bulk || e0 >= vse) continue;
-            uint4 v;
-            if (e0 >= len) {
-                v = ES == 2 ? make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u)
-                            : make_uint4(0xFF800000u, 0xFF800000u, 0xFF800000u, 0xFF800000u);
-            } else {
-                v = load_straddle<Tin>(sl, reinterpret_cast<const Tin*>(lv.ptr[l]) + b * lv.bs[l] + i * lv.ld[l] + base,
-                                       e0, len_bulk, len);
-            }
+            const int e0 = vec_index<Tin>(w, lane, jv);
+            if (e0 + VEC <= len_bulk || e0 >= len) continue;
+            const uint4 v = load_straddle<Tin>(
+                sl, reinterpret_cast<const Tin*>(lv.ptr[l]) + b * lv.bs[l] + i * lv.ld[l] + base, e0, len_bulk, len);
             *reinterpret_cast<uint4*>(sl + e0) = v;
         }
     }
@@ -215,433 +231,631 @@ __device__ __noinline__ void repair_stage(Tin* stage, const LevelDesc& lv, int64
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// e = 2^((z - m) log2 e) of one thread's CET elements of one row (y = z - m returned too);
+// `clamp`: the -1e30 clamp first (-inf -> p = 0 without 0 * inf), NaN kept.
+template <typename Tin>
+__device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, float* e, float2* y) {
+    const float nm = -m;
+    const float2 nm2 = make_float2(nm, nm);
+    const float2 l2e = make_float2(LOG2E, LOG2E);
+#pragma unroll
+    for (int pp = 0; pp < CET / 2; ++pp) {
+        float2 yy;
+        if (sizeof(Tin) == 2) {
+            uint32_t w = word_of(raw[pp >> 2], pp & 3);
+            if (clamp) w = clamp_bf16x2(w);
+            yy = make_float2(bf16lo_add(w, nm), bf16hi_add(w, nm));
+        } else {
+            const uint4& r = raw[pp >> 1];
+            float2 xv = (pp & 1) ? make_float2(__uint_as_float(r.z), __uint_as_float(r.w))
+                                 : make_float2(__uint_as_float(r.x), __uint_as_float(r.y));
+            xv.x = clamp1(xv.x);
+            xv.y = clamp1(xv.y);
+            yy = __fadd2_rn(xv, nm2);
+        }
+        const float2 t = __fmul2_rn(yy, l2e);
+        e[2 * pp] = ex2f(t.x);
+        e[2 * pp + 1] = ex2f(t.y);
+        y[pp] = yy;
+    }
+}
+
+// e and y = z - m of half h (8 of the thread's 16 elements) of one row of a ring stage
+template <typename Tin>
+__device__ __forceinline__ void half_exp(const Tin* row, int rg, int lane, int h, float m, bool clamp, float* e,
+                                         float2* y) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    constexpr int NVH = 8 / VEC;        // vectors per half: 1 (bf16) or 2 (f32)
+    uint4 raw[NVH];
+#pragma unroll
+    for (int jv = 0; jv < NVH; ++jv)
+        raw[jv] = *reinterpret_cast<const uint4*>(row + vec_index<Tin>(rg, lane, h * NVH + jv));
+    const float nm = -m;
+    const float2 nm2 = make_float2(nm, nm);
+    const float2 l2e = make_float2(LOG2E, LOG2E);
+#pragma unroll
+    for (int pp = 0; pp < 4; ++pp) {
+        float2 yy;
+        if (sizeof(Tin) == 2) {
+            uint32_t w = word_of(raw[0], pp);
+            if (clamp) w = clamp_bf16x2(w);
+            yy = make_float2(bf16lo_add(w, nm), bf16hi_add(w, nm));
+        } else {
+            const uint4& r = raw[pp >> 1];
+            float2 xv = (pp & 1) ? make_float2(__uint_as_float(r.z), __uint_as_float(r.w))
+                                 : make_float2(__uint_as_float(r.x), __uint_as_float(r.y));
+            xv.x = clamp1(xv.x);
+            xv.y = clamp1(xv.y);
+            yy = __fadd2_rn(xv, nm2);
+        }
+        const float2 t = __fmul2_rn(yy, l2e);
+        e[2 * pp] = ex2f(t.x);
+        e[2 * pp + 1] = ex2f(t.y);
+        y[pp] = yy;
+    }
+}
+// element index (within the slice) of element 2 pp (+1) of half h of pass-1 thread (rg, lane)
+template <typename Tin>
+__device__ __forceinline__ int half_index(int rg, int lane, int h, int pp) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    constexpr int NVH = 8 / VEC;
+    return vec_index<Tin>(rg, lane, h * NVH + (2 * pp) / VEC) + (2 * pp) % VEC;
+}
+__device__ __forceinline__ void tm_st8(uint32_t ta, const float* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
+}
+
+#ifdef MSD_PROF
+#define PROF_DECL long long _pa[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long _pt = clock64(); long long _pn = 0;
+#define PROF(k) { const long long _t = clock64(); _pa[k] += _t - _pt; _pt = _t; }
+#define PROF_ITEM ++_pn;
+#define PROF_FLUSH(role) if (p.trace && lane == 0) { for (int _k = 0; _k < 8; ++_k) atomicAdd(p.trace + (role) * 16 + _k, (unsigned long long)_pa[_k]); atomicAdd(p.trace + (role) * 16 + 15, (unsigned long long)_pn); }
+#else
+#define PROF_DECL
+#define PROF(k)
+#define PROF_ITEM
+#define PROF_FLUSH(role)
+#endif
+
+// Incremental ring / pattern position of item j (no runtime integer division in the loops:
+// it would issue on the busy MUFU pipe).
+struct Cursor {
+    int j = 0;
+    int st = 0, sph = 0;           // ring stage, its phase parity
+    int pr = 0;                    // position within the item pattern period
+    int q = 0, tph = 0, tj = 0;    // TMEM slot of the next T item, its phase parity, T-item count
+    __device__ __forceinline__ bool isT(int PT) const { return pr < PT; }
+    __device__ __forceinline__ void next(int S, int PP, int PT, int NT) {
+        if (pr < PT) {
+            ++tj;
+            if (++q == NT) { q = 0; tph ^= 1; }
+        }
+        if (++pr == PP) pr = 0;
+        if (++st == S) { st = 0; sph ^= 1; }
+        ++j;
+    }
+};
+
 template <typename Tin, int L, bool GREEDY>
 __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
-    constexpr int NV = CET / VEC;           // 1 (bf16) or 2 (f32) vectors per thread and row
+    constexpr int NV = CET / VEC;           // 2 (bf16) or 4 (f32) vectors per thread and row
     constexpr int ES = (int)sizeof(Tin);
-    constexpr int NT = core_tslots(L);                       // TMEM item slots
-    constexpr int NSS = core_sslots(L, ES, (int)sizeof(Ctl<L>)); // shared-memory item slots
-    constexpr int NR = NT + NSS;
-    static_assert(NR <= NRMAX && NT >= 2, "item slots");
+    constexpr int NT = core_tslots(L);      // TMEM item slots
+    static_assert(NT <= NTMAX && NT >= 2, "item slots");
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int S = core_stages(L, ES);
-    Tin* ring = reinterpret_cast<Tin*>(smem);
-    Ctl<L>& c = *reinterpret_cast<Ctl<L>*>(smem + align_up((size_t)S * L * VS * ES, 128));
-    // shared-memory exponential slots: [slot][row][k][pass-1 thread] (conflict-free)
-    float* xslot = reinterpret_cast<float*>(smem + align_up((size_t)S * L * VS * ES, 128) + align_up(sizeof(Ctl<L>), 128));
+    Ctl<L>& c = *reinterpret_cast<Ctl<L>*>(smem);
+    Tin* ring = reinterpret_cast<Tin*>(smem + align_up(sizeof(Ctl<L>), 128));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int C = p.C;
     const int VSe = p.VSe;
+    const int RS = p.rs;                    // ring row stride (entries)
+    const int S = p.stages;
+    const int PP = p.pat_p, PT = p.pat_t;
+    const int nact = min(NCW, (VSe + WCH - 1) / WCH);   // element regions (pass-1 warps) with data
+    const int np2 = min(NCW2, nact);                     // pass-2 warps with data
     // group scheduling: the grid is k groups of C CTAs; CTA (group, s) handles slice s of
     // units group, group + k, ... -- a unit's C slices always run together on one group
     const int kgrp = gridDim.x / C;
     const int grp = blockIdx.x / C, sfix = blockIdx.x % C;
     const int n_my = grp < kgrp && grp < p.U ? (p.U - grp + kgrp - 1) / kgrp : 0;
 
-    // the ring tail [VSe, VS) of every row is never written by the bulk copies: -inf once, so
-    // that clean items load whole vectors unconditionally
-    for (int e = tid; e < S * L * (VS - VSe); e += blockDim.x) {
-        const int row = e / (VS - VSe);
-        ring[(size_t)row * VS + VSe + (e - row * (VS - VSe))] = (Tin)(-INFINITY);
+    // the ring tail [VSe, RS) of every row is never written by the bulk copies: the pad value
+    // once, so that the last active warp loads whole vectors unconditionally
+    {
+        uint32_t* r32 = reinterpret_cast<uint32_t*>(ring);
+        const int per_row = (RS - VSe) * ES / 4;
+        for (int e = tid; e < S * L * per_row; e += blockDim.x) {
+            const int row = e / per_row;
+            r32[(size_t)row * (RS * ES / 4) + VSe * ES / 4 + (e - row * per_row)] = 0xF1F1F1F1u;
+        }
     }
     if (warp == W_PROD) {
         if (lane == 0) {
-            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], NCW); }
-            for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], NCW); mbar_init(&c.r1_empty[r], 1); }
-            for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], NCW); mbar_init(&c.r2_empty[r], 1); }
-            for (int q = 0; q < NR; ++q) {
-                mbar_init(&c.rowf_full[q], 1);
-                mbar_init(&c.rowf_empty[q], NCW);
-                mbar_init(&c.tm_full[q], NCW);
-                mbar_init(&c.tm_empty[q], NCW);
+            // empty: one arrival per region (pass-1 warps for T items, pass-2 warps for R items)
+            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], nact); }
+            for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], nact); mbar_init(&c.r1_empty[r], 1); }
+            for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], np2); mbar_init(&c.r2_empty[r], 1); }
+            for (int k = 0; k < NQ; ++k) {
+                mbar_init(&c.rowf_full[k], 1);
+                mbar_init(&c.rowf_empty[k], np2);
+                mbar_init(&c.pub[k], 1);
             }
+            for (int q = 0; q < NT; ++q) { mbar_init(&c.tm_full[q], nact); mbar_init(&c.tm_empty[q], np2); }
             fence_mbar_init();
         }
         __syncwarp();
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&c.taddr)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    if (tid < NQ) c.clampw[tid] = 0u;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
     auto stamp = [&](int j, int k) {
-        if (p.trace && !(p.dbg & 64)) p.trace[((int64_t)(grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
+#if defined(MSD_TRACE) && !defined(MSD_PROF)
+        if (p.trace) p.trace[((int64_t)(grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
+#endif
     };
-    // (no runtime integer division on the hot loops: it would issue on the busy MUFU pipe)
-    auto item = [&](int j, int64_t& u, int& s, int64_t& b, int64_t& i) {
+    auto item = [&](int j, int64_t& u, int64_t& b, int64_t& i) {
         const uint32_t uu = (uint32_t)(grp + j * kgrp);
         const uint32_t bb = __umulhi(uu, p.kinv);
         u = uu;
-        s = sfix;
         b = bb;
         i = uu - bb * (uint32_t)p.K;
     };
+    // TMEM column base of region w (lane quadrant w & 3, column block w >> 2)
+    auto tcol = [&](int w) { return c.taddr + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((w >> 2) * TCOLS); };
+    const int s = sfix;
+    const int64_t base = (int64_t)s * VSe;
+    const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
+    const int len_bulk = (len * ES) / 16 * 16 / ES;
 
-    const bool dbg_idle = p.dbg != 0 && warp >= NCW && (warp != W_PROD || (p.dbg & 32));
-    if (dbg_idle) {
-    } else if (warp < NCW) {
+    const bool p1only = (p.dbg & 1) != 0;   // debug: pass 1 + TMA ring only (results invalid)
+    if (p1only && warp != W_PROD && warp < W_P1) {
+    } else if (warp >= W_P1) {
         // ================================================================ pass-1 warps
-        const uint32_t tbase = c.taddr + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 256);
-#ifdef MSD_PHASE_PROF
-        long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#endif
-        for (int j = 0; j < n_my; ++j) {
-            int64_t u, b, i;
-            int s;
-            item(j, u, s, b, i);
-            const int st = (int)(j % S);
-            const int q = (int)(j % NR);
-            const int r1 = (int)(j % R1);
-            const int64_t base = (int64_t)s * VSe;
-            const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
-            const int len_bulk = (len * ES) / 16 * 16 / ES;
-#ifdef MSD_PHASE_PROF
-            long long ck0 = clock64();
-#endif
-            if (!(p.dbg & 32)) mbar_wait(&c.full[st], (uint32_t)((j / S) & 1));
-#ifdef MSD_PHASE_PROF
-            long long ck1 = clock64();
-#endif
-            if (tid == 0) stamp(j, 1);
-            uint4 raw[L][NV];
-            float tmax[L];
-            // a row length that is not a multiple of 16 bytes: patch the straddling vector
-            if (len_bulk != len) repair_stage<Tin, L, NV>(ring + (size_t)st * L * VS, p.lv, b, i, base, tid, len_bulk, len, VSe);
-            // every vector from the ring ([VSe, VS) holds -inf from the prologue)
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                const Tin* sl = ring + ((size_t)st * L + l) * VS;
-#pragma unroll
-                for (int jv = 0; jv < NV; ++jv) raw[l][jv] = *reinterpret_cast<const uint4*>(sl + (jv * CTH + tid) * VEC);
-            }
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                float tm = -INFINITY;
-                if (ES == 2) {
-                    uint32_t mx = 0xFF80FF80u;
-#pragma unroll
-                    for (int jv = 0; jv < NV; ++jv) {
-                        uint4& r = raw[l][jv];
-                        r.x = clamp_bf16x2(r.x); r.y = clamp_bf16x2(r.y);
-                        r.z = clamp_bf16x2(r.z); r.w = clamp_bf16x2(r.w);
-                        mx = max_nan_bf16x2(mx, max_nan_bf16x2(max_nan_bf16x2(r.x, r.y), max_nan_bf16x2(r.z, r.w)));
-                    }
-                    tm = fmaxf(bf16lo(mx), bf16hi(mx));
-                } else {
-#pragma unroll
-                    for (int jv = 0; jv < NV; ++jv) {
-                        float xs[4];
-                        unpack_clamped<float>(raw[l][jv], xs);
-                        raw[l][jv] = make_uint4(__float_as_uint(xs[0]), __float_as_uint(xs[1]),
-                                                __float_as_uint(xs[2]), __float_as_uint(xs[3]));
-                        tm = fmaxf(tm, fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])));
-                    }
-                }
-                tmax[l] = tm;
-            }
-            // the slice is in registers now: hand the ring stage back to the producer
-            __syncwarp();
-            if (lane == 0 && !(p.dbg & 32)) mbar_arrive(&c.empty[st]);
-            // per-warp max of all rows, the shuffle chains interleaved
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) tmax[l] = fmaxf(tmax[l], __shfl_xor_sync(0xffffffffu, tmax[l], o));
-            }
-#ifdef MSD_PHASE_PROF
-            long long ck2 = clock64();
-#endif
-            if (p.dbg & 8) continue;   // debug: TMA ring only
-            if (j >= NR && !p.dbg) {   // slot q (TMEM and wmx) must have been released by the pass-2 warps
-                mbar_wait(&c.tm_empty[q], (uint32_t)(((j / NR) - 1) & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            }
-            if (tid == 0) stamp(j, 2);
-#ifdef MSD_PHASE_PROF
-            long long ck3 = clock64();
-#endif
-            if (lane == 0) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) c.wmx[q][l][warp] = tmax[l];
-            }
-            float Sv[L], Kv[L];
-            int am[L];
-            float2 yprev[CET / 2];
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                // y = z - m_w exactly (bf16 / clamped inputs), e = 2^(y log2 e) on the MUFU; the
-                // rest in packed fp32 pairs (FADD2 / FMUL2 / FFMA2): sum e and the KL numerator
-                // sum e (y_l - y_{l-1}) = sum e ((z_l - z_{l-1}) - (m_l - m_{l-1}))
-                const float2 nm = make_float2(-tmax[l], -tmax[l]);
-                const float2 l2e = make_float2(LOG2E, LOG2E);
-                const float2 neg1 = make_float2(-1.f, -1.f);
-                float e[CET];
-                float2 s2 = make_float2(0.f, 0.f), k2 = make_float2(0.f, 0.f);
-                am[l] = 0x7fffffff;
-#pragma unroll
-                for (int pp = 0; pp < CET / 2; ++pp) {
-                    const float2 xv = elem_pair<Tin>(raw[l][(2 * pp) / VEC], pp % (VEC / 2));
-                    const float2 y = __fadd2_rn(xv, nm);
-                    const float2 t = __fmul2_rn(y, l2e);
-                    const float2 ev = make_float2(ex2f(t.x), ex2f(t.y));
-                    e[2 * pp] = ev.x;
-                    e[2 * pp + 1] = ev.y;
-                    s2 = __fadd2_rn(s2, ev);
-                    if (l > 0) k2 = __ffma2_rn(ev, __ffma2_rn(yprev[pp], neg1, y), k2);
-                    yprev[pp] = y;
-                    if (GREEDY) {
-                        const int k0 = 2 * pp;
-                        const int i0 = (int)(base + ((k0 / VEC) * CTH + tid) * VEC + (k0 % VEC));
-                        if (xv.x == tmax[l]) am[l] = min(am[l], i0);
-                        if (xv.y == tmax[l]) am[l] = min(am[l], i0 + 1);
-                    }
-                }
-                if (q < NT) {
-                    tm_st16(tbase + (uint32_t)(q * CET * L + l * CET), e);
-                } else {
-                    float* xs = xslot + ((size_t)((q - NT) * L + l) * CET) * CTH + tid;
-#pragma unroll
-                    for (int k = 0; k < CET; ++k) xs[k * CTH] = e[k];
-                }
-                Sv[l] = s2.x + s2.y;
-                Kv[l] = k2.x + k2.y;
-            }
-#ifdef MSD_PHASE_PROF
-            long long ck4 = clock64();
-#endif
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                Sv[l] = fold4(Sv[l]);
-                if (l > 0) Kv[l] = fold4(Kv[l]);
-            }
-            if (GREEDY) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) am[l] = warp_min_i(am[l]);
-            }
-#ifdef MSD_PHASE_PROF
-            long long ck5 = clock64();
-#endif
-            if (j >= R1 && !p.dbg) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
-            if (lane < NSUB) {
+        // Two groups of NCW warps take alternate items, so one group's reductions and barrier
+        // waits overlap the other group's exponentials.  Reference: the warp maximum of the
+        // row (the dominant entries then have |z - m| small, so the fp32 exponent argument
+        // keeps full relative accuracy).  Rows are processed in two 8-element halves.
+        const int g1 = (warp - W_P1) / NCW;
+        const int rg = (warp - W_P1) % NCW;     // element region
+        if (rg < nact) {
+            PROF_DECL
+            const uint32_t tbase = tcol(rg);
+            Cursor cu;
+            for (int x = 0; x < g1; ++x) cu.next(S, PP, PT, NT);
+            for (; cu.j < n_my;) {
+                const int j = cu.j;
+                int64_t u, b, i;
+                item(j, u, b, i);
+                const bool isT = cu.isT(PT);
+                const int q = cu.q;
+                const int k = j & (NQ - 1);
+                const int r1 = j & (R1 - 1);
+                Tin* stage = ring + (size_t)cu.st * L * RS;
+                mbar_wait(&c.full[cu.st], (uint32_t)cu.sph);
+                PROF(0)
+                if (rg == 0 && lane == 0) stamp(j, 1);
+                // a row length that is not a multiple of 16 bytes: patch the straddling vector
+                if (len_bulk != len) repair_stage<Tin, L, NV>(stage, RS, p.lv, b, i, base, rg, lane, len_bulk, len);
+                // per-thread then per-warp max of every row (NaN-propagating)
+                float wm[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
-                    c.r1S[r1][l][warp][lane] = Sv[l];
-                    c.r1K[r1][l][warp][lane] = Kv[l];
-                }
-                if (GREEDY && lane == 0) {
+                    float tm = -INFINITY;
 #pragma unroll
-                    for (int l = 0; l < L; ++l) c.r1A[r1][l][warp] = am[l];
+                    for (int jv = 0; jv < NV; ++jv) {
+                        const uint4 r = *reinterpret_cast<const uint4*>(stage + (size_t)l * RS + vec_index<Tin>(rg, lane, jv));
+                        if (ES == 2) {
+                            const uint32_t mx = max_nan_bf16x2(max_nan_bf16x2(r.x, r.y), max_nan_bf16x2(r.z, r.w));
+                            tm = max_nan_f32(tm, max_nan_f32(bf16lo(mx), bf16hi(mx)));
+                        } else {
+                            tm = max_nan_f32(max_nan_f32(tm, max_nan_f32(__uint_as_float(r.x), __uint_as_float(r.y))),
+                                             max_nan_f32(__uint_as_float(r.z), __uint_as_float(r.w)));
+                        }
+                    }
+                    wm[l] = redux_max_nan(tm);
                 }
-            }
-#ifdef MSD_PHASE_PROF
-            long long ck6 = clock64();
-#endif
-            tm_wait_st();
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (tid == 0) stamp(j, 3);
-#ifdef MSD_PHASE_PROF
-            if (p.dbg & 64) {   // debug: pass-1 phase cycle profile (register accumulators)
-                long long ck7 = clock64();
-                pc[0] += ck1 - ck0; pc[1] += ck2 - ck1; pc[2] += ck3 - ck2; pc[3] += ck4 - ck3;
-                pc[4] += ck5 - ck4; pc[5] += ck6 - ck5; pc[6] += ck7 - ck6; pc[7] += 1;
-            }
-#endif
-            if (lane == 0) {
-                if (!p.dbg) {
+                // record slot k free (pass 2 of item j - NQ has read it), TMEM slot q free,
+                // record ring slot r1 free
+                if (j >= NQ && !p1only) mbar_wait(&c.rowf_empty[k], (uint32_t)(((j / NQ) - 1) & 1));
+                if (isT && cu.tj >= NT && !p1only) {
+                    mbar_wait(&c.tm_empty[q], (uint32_t)(cu.tph ^ 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                if (j >= R1 && !p1only) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
+                if (rg == 0 && lane == 0) stamp(j, 2);
+                PROF(1)
+                float Sv[L], Kv[L];
+                int am[L];
+                // one pass over the thread's elements, half-major (all rows of half 0, then of
+                // half 1); e parked in TMEM (T items)
+                auto run = [&](bool clamp) {
+                    float2 s2[L], k2[L];
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        s2[l] = k2[l] = make_float2(0.f, 0.f);
+                        am[l] = 0x7fffffff;
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        float2 yprev[4];
+#pragma unroll
+                        for (int l = 0; l < L; ++l) {
+                            float e[8];
+                            float2 y[4];
+                            half_exp<Tin>(stage + (size_t)l * RS, rg, lane, h, wm[l], clamp, e, y);
+                            const float2 e01 = __fadd2_rn(make_float2(e[0], e[1]), make_float2(e[2], e[3]));
+                            const float2 e23 = __fadd2_rn(make_float2(e[4], e[5]), make_float2(e[6], e[7]));
+                            s2[l] = __fadd2_rn(s2[l], __fadd2_rn(e01, e23));
+                            if (l > 0) {
+                                const float2 neg1 = make_float2(-1.f, -1.f);
+                                float2 ka = __fmul2_rn(make_float2(e[0], e[1]), __ffma2_rn(yprev[0], neg1, y[0]));
+                                float2 kb = __fmul2_rn(make_float2(e[2], e[3]), __ffma2_rn(yprev[1], neg1, y[1]));
+                                ka = __ffma2_rn(make_float2(e[4], e[5]), __ffma2_rn(yprev[2], neg1, y[2]), ka);
+                                kb = __ffma2_rn(make_float2(e[6], e[7]), __ffma2_rn(yprev[3], neg1, y[3]), kb);
+                                k2[l] = __fadd2_rn(k2[l], __fadd2_rn(ka, kb));
+                            }
+#pragma unroll
+                            for (int pp = 0; pp < 4; ++pp) {
+                                yprev[pp] = y[pp];
+                                if (GREEDY) {
+                                    const int ib = (int)base + half_index<Tin>(rg, lane, h, pp);
+                                    if (y[pp].x == 0.f) am[l] = min(am[l], ib);
+                                    if (y[pp].y == 0.f) am[l] = min(am[l], ib + 1);
+                                }
+                            }
+                            if (isT) tm_st8(tbase + (uint32_t)(q * CET * L + l * CET + h * 8), e);
+                        }
+                    }
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        Sv[l] = s2[l].x + s2[l].y;
+                        Kv[l] = k2[l].x + k2[l].y;
+                    }
+                };
+                // fast path: bf16 rows whose warp maxima are finite (no masked / NaN / +inf
+                // chunk); -inf entries inside a finite chunk are caught by the finiteness check.
+                // Otherwise (and for f32 logits): the -1e30 clamp.
+                bool fast = ES == 2;
+#pragma unroll
+                for (int l = 0; l < L; ++l) fast = fast && (wm[l] > NEG_MASKED) && (wm[l] < INFINITY);
+                if (fast) {
+                    run(false);
+                    bool ok = true;
+#pragma unroll
+                    for (int l = 0; l < L; ++l) ok = ok && isfinite(Sv[l]) && isfinite(Kv[l]);
+                    fast = __all_sync(0xffffffffu, ok);
+                    if (!fast && isT) tm_wait_st();
+                }
+                if (!fast) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        float tm = -INFINITY;
+#pragma unroll
+                        for (int jv = 0; jv < NV; ++jv) {
+                            float xs[VEC];
+                            unpack_clamped<Tin>(*reinterpret_cast<const uint4*>(stage + (size_t)l * RS + vec_index<Tin>(rg, lane, jv)), xs);
+#pragma unroll
+                            for (int kk = 0; kk < VEC; ++kk) tm = max_nan_f32(tm, xs[kk]);
+                        }
+                        wm[l] = redux_max_nan(tm);
+                    }
+                    run(true);
+                }
+                PROF(2)
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    Sv[l] = fold4(Sv[l]);
+                    if (l > 0) Kv[l] = fold4(Kv[l]);
+                }
+                if (GREEDY) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) am[l] = redux_min_s32(am[l]);
+                }
+                // a T item's slice has been consumed: hand the ring stage back to the producer
+                // (an R item's stage is released by pass 2)
+                __syncwarp();
+                if (lane == 0) {
+                    if (isT || p1only) mbar_arrive(&c.empty[cu.st]);
+#pragma unroll
+                    for (int l = 0; l < L; ++l) c.wmx[k][l][rg] = wm[l];
+                    const uint32_t bit = 1u << rg;
+                    if (fast) atomicAnd(&c.clampw[k], ~bit);
+                    else atomicOr(&c.clampw[k], bit);
+                }
+                PROF(3)
+                if (lane < NSUB) {
+#pragma unroll
+                    for (int l = 0; l < L; ++l) {
+                        c.r1S[r1][l][rg][lane] = Sv[l];
+                        c.r1K[r1][l][rg][lane] = Kv[l];
+                    }
+                    if (GREEDY && lane == 0) {
+#pragma unroll
+                        for (int l = 0; l < L; ++l) c.r1A[r1][l][rg] = am[l];
+                    }
+                }
+                PROF(4)
+                if (isT) {
+                    tm_wait_st();
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                }
+                __syncwarp();
+                if (rg == 0 && lane == 0) stamp(j, 3);
+                if (lane == 0 && !p1only) {
                     mbar_arrive(&c.r1_full[r1]);
-                    mbar_arrive(&c.tm_full[q]);
+                    if (isT) mbar_arrive(&c.tm_full[q]);
                 }
+                PROF(5)
+                PROF_ITEM
+                for (int x = 0; x < NG1; ++x) cu.next(S, PP, PT, NT);
             }
+            PROF_FLUSH(0)
         }
-#ifdef MSD_PHASE_PROF
-        if ((p.dbg & 64) && p.trace && lane == 0)
-            for (int k = 0; k < 8; ++k) atomicAdd(p.trace + warp * 8 + k, (unsigned long long)pc[k]);
-#endif
-    } else if (warp < W_PROD) {
+    } else if (warp >= W_P2) {
         // ================================================================ pass-2 warps
-        // warp NCW + w reads the TMEM lanes / columns written by pass-1 warp w
-        const int w = warp - W_P2;
-        const uint32_t tbase = c.taddr + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((w >> 2) * 256);
-        for (int j = 0; j < n_my; ++j) {
-            const int q = (int)(j % NR);
-            const int r2 = (int)(j % R2);
-            mbar_wait(&c.rowf_full[q], (uint32_t)((j / NR) & 1));
-            if (w == 0 && lane == 0) stamp(j, 11);
-            float rh[L], sc[L];
+        // warp W_P2 + v handles regions v and v + NCW2 (same TMEM lane quadrant)
+        const int v = warp - W_P2;
+        if (v < np2) {
+            PROF_DECL
+            const bool two = v + NCW2 < nact;
+            Cursor cu;
+            for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
+                const int j = cu.j;
+                const bool isT = cu.isT(PT);
+                const int q = cu.q;
+                const int k = j & (NQ - 1);
+                const int r2 = j & (R2 - 1);
+                mbar_wait(&c.rowf_full[k], (uint32_t)((j / NQ) & 1));
+                PROF(0)
+                float rh[2][L], sc[2][L], wm[2][L];
+                const uint32_t cw = c.clampw[k];
 #pragma unroll
-            for (int l = 1; l < L; ++l) {
-                rh[l] = c.rowf[q][l][w].rho;
-                sc[l] = c.rowf[q][l][w].scale;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c.rowf_empty[q]);
-            mbar_wait(&c.tm_full[q], (uint32_t)((j / NR) & 1));
-            if (w == 0 && lane == 0) stamp(j, 12);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            float ev[L][CET];
-            if (q < NT) {
+                for (int h = 0; h < 2; ++h) {
+                    const int w = v + h * NCW2;
 #pragma unroll
-                for (int l = 0; l < L; ++l) tm_ld16(tbase + (uint32_t)(q * CET * L + l * CET), ev[l]);
-                tm_wait_ld();
-            } else {
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    const float* xs = xslot + ((size_t)((q - NT) * L + l) * CET) * CTH + w * 32 + lane;
-#pragma unroll
-                    for (int k = 0; k < CET; ++k) ev[l][k] = xs[k * CTH];
+                    for (int l = 0; l < L; ++l) {
+                        rh[h][l] = sc[h][l] = 0.f;
+                        wm[h][l] = 0.f;
+                        if (h == 0 || two) {
+                            if (l > 0) {
+                                rh[h][l] = c.rowf[k][l][w].rho;
+                                sc[h][l] = c.rowf[k][l][w].scale;
+                            }
+                            wm[h][l] = c.wmx[k][l][w];
+                        }
+                    }
                 }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c.tm_empty[q]);
-            float acc[L];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&c.rowf_empty[k]);
+                float acc[L];
 #pragma unroll
-            for (int l = 1; l < L; ++l) {
-                float a = 0.f;
+                for (int l = 0; l < L; ++l) acc[l] = 0.f;
+                // residual of the pair (l-1, l) of region h: sum max(e_l - rho e_{l-1}, 0), scaled
+                auto pair = [&](int h, int l, const float* ea, const float* eb) {
+                    const float2 nr = make_float2(-rh[h][l], -rh[h][l]);
+                    float2 a2 = make_float2(0.f, 0.f), a2b = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int k = 0; k < CET; ++k) {
-                    a += fmaxf(fmaf(-ev[l - 1][k], rh[l], ev[l][k]), 0.f);
+                    for (int kk = 0; kk < CET; kk += 2) {
+                        float2 t = __ffma2_rn(make_float2(eb[kk], eb[kk + 1]), nr, make_float2(ea[kk], ea[kk + 1]));
+                        t.x = fmaxf(t.x, 0.f);
+                        t.y = fmaxf(t.y, 0.f);
+                        if (kk & 2) a2b = __fadd2_rn(a2b, t);
+                        else a2 = __fadd2_rn(a2, t);
+                    }
+                    a2 = __fadd2_rn(a2, a2b);
+                    acc[l] = fmaf(a2.x + a2.y, sc[h][l], acc[l]);
+                };
+                if (isT) {
+                    mbar_wait(&c.tm_full[q], (uint32_t)cu.tph);
+                    if (v == 0 && lane == 0) stamp(j, 12);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    PROF(1)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 0 || two) {
+                            const uint32_t tb = tcol(v + h * NCW2) + (uint32_t)(q * CET * L);
+                            float ea[CET], eb[CET];
+                            tm_ld16(tb, eb);
+#pragma unroll
+                            for (int l = 1; l < L; ++l) {
+                                tm_ld16(tb + (uint32_t)(l * CET), ea);
+                                tm_wait_ld();
+                                pair(h, l, ea, eb);
+#pragma unroll
+                                for (int kk = 0; kk < CET; ++kk) eb[kk] = ea[kk];
+                            }
+                        }
+                    }
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&c.tm_empty[q]);
+                    PROF(2)
+                } else {
+                    // R item: recompute e from the kept ring stage (already complete: full[st]
+                    // cannot advance before the stage is released here)
+                    mbar_wait(&c.full[cu.st], (uint32_t)cu.sph);
+                    if (v == 0 && lane == 0) stamp(j, 12);
+                    PROF(1)
+                    const Tin* stage = ring + (size_t)cu.st * L * RS;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (h == 0 || two) {
+                            const int w = v + h * NCW2;
+                            const bool clamp = ((cw >> w) & 1u) || ES == 4;
+                            float eprev[CET];
+#pragma unroll
+                            for (int l = 0; l < L; ++l) {
+                                uint4 raw[NV];
+#pragma unroll
+                                for (int jv = 0; jv < NV; ++jv)
+                                    raw[jv] = *reinterpret_cast<const uint4*>(stage + (size_t)l * RS + vec_index<Tin>(w, lane, jv));
+                                float e[CET];
+                                float2 y[CET / 2];
+                                row_exp<Tin>(raw, wm[h][l], clamp, e, y);
+                                if (l > 0) pair(h, l, e, eprev);
+#pragma unroll
+                                for (int kk = 0; kk < CET; ++kk) eprev[kk] = e[kk];
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cnt(&c.empty[cu.st], two ? 2u : 1u);
+                    PROF(2)
                 }
-                acc[l] = a;
-            }
 #pragma unroll
-            for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
-            if (j >= R2) mbar_wait(&c.r2_empty[r2], (uint32_t)(((j / R2) - 1) & 1));
-            if (lane < NSUB) {
+                for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
+                PROF(3)
+                if (j >= R2) mbar_wait(&c.r2_empty[r2], (uint32_t)(((j / R2) - 1) & 1));
+                if (lane < NSUB) {
 #pragma unroll
-                for (int l = 1; l < L; ++l) c.r2R[r2][l][w][lane] = acc[l];
+                    for (int l = 1; l < L; ++l) c.r2R[r2][l][v][lane] = acc[l];
+                }
+                __syncwarp();
+                if (v == 0 && lane == 0) stamp(j, 13);
+                if (lane == 0) mbar_arrive(&c.r2_full[r2]);
+                PROF(4)
+                PROF_ITEM
             }
-            if (lane == 0) {
-#pragma unroll
-                for (int l = 1; l < L; ++l) c.r2scale[r2][l][w] = sc[l];
-            }
-            __syncwarp();
-            if (w == 0 && lane == 0) stamp(j, 13);
-            if (lane == 0) mbar_arrive(&c.r2_full[r2]);
+            PROF_FLUSH(1)
         }
     } else if (warp == W_PROD) {
         // ================================================================ TMA producer
+        PROF_DECL
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            for (int j = 0; j < n_my; ++j) {
-                const int st = (int)(j % S);
-                if (j >= S) mbar_wait(&c.empty[st], (uint32_t)(((j / S) - 1) & 1));
+            const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
+            // the last slice of a row: pad [bulk end, VSe) from the constant pad buffer so
+            // the pass-1 loads stay unconditional (the copy engine does the fill)
+            const uint32_t pad = (uint32_t)(VSe * ES) - bytes;
+            Cursor cu;
+            for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
+                const int j = cu.j;
+                if (j >= S) mbar_wait(&c.empty[cu.st], (uint32_t)(cu.sph ^ 1));
+                PROF(0)
                 int64_t u, b, i;
-                int s;
-                item(j, u, s, b, i);
-                const int64_t len = max((int64_t)0, min((int64_t)VSe, p.V - (int64_t)s * VSe));
-                const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
-                // the last slice of a row: pad [bulk end, VSe) from the constant pad buffer so
-                // the pass-1 loads stay unconditional (the copy engine does the fill)
-                const uint32_t pad = (uint32_t)(VSe * ES) - bytes;
+                item(j, u, b, i);
                 stamp(j, 0);
-                mbar_arrive_expect_tx(&c.full[st], (bytes + pad) * L);
+                mbar_arrive_expect_tx(&c.full[cu.st], (bytes + pad) * L);
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
-                    Tin* dst = ring + ((size_t)st * L + l) * VS;
+                    Tin* dst = ring + ((size_t)cu.st * L + l) * RS;
                     if (bytes) {
-                        const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] +
-                                         i * p.lv.ld[l] + (int64_t)s * VSe;
-                        bulk_g2s(dst, src, bytes, &c.full[st], pol);
+                        const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] + i * p.lv.ld[l] + base;
+                        bulk_g2s(dst, src, bytes, &c.full[cu.st], pol);
                     }
-                    if (pad) bulk_g2s(reinterpret_cast<unsigned char*>(dst) + bytes, p.pad, pad, &c.full[st], pol);
+                    if (pad) bulk_g2s(reinterpret_cast<unsigned char*>(dst) + bytes, p.pad, pad, &c.full[cu.st], pol);
                 }
+                PROF(1)
+                PROF_ITEM
             }
         }
+        PROF_FLUSH(5)
     } else if (warp == W_PUB) {
         // ================================================================ publisher
-        // lane = 4 * w + t: pass-1 warp w, record t (of NSUB)
+        // lane = 4 w + t: region w, sub-record t.  Factors 2^((R_w - R_s) log2 e) relative to the
+        // largest reference R_s (all 1 when every warp used the slice reference).
+        PROF_DECL
         const int w = lane >> 2, t = lane & 3;
+        const bool act = w < nact;
         for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
-            int s;
-            item(j, u, s, b, i);
-            const int q = (int)(j % NR);
-            const int r1 = (int)(j % R1);
+            item(j, u, b, i);
+            const int k = j & (NQ - 1);
+            const int r1 = j & (R1 - 1);
             mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
+            PROF(0)
             float Sw[L], Kw[L], wm[L];
             int aw[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                Sw[l] = c.r1S[r1][l][w][t];
-                Kw[l] = c.r1K[r1][l][w][t];
-                wm[l] = c.wmx[q][l][w];
-                aw[l] = (GREEDY && t == 0) ? c.r1A[r1][l][w] : 0x7fffffff;
+                Sw[l] = act ? c.r1S[r1][l][w][t] : 0.f;
+                Kw[l] = act ? c.r1K[r1][l][w][t] : 0.f;
+                wm[l] = act ? c.wmx[k][l][w] : -INFINITY;
+                aw[l] = (GREEDY && act && t == 0) ? c.r1A[r1][l][w] : 0x7fffffff;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
-            // slice combine in fp32 (per-warp factors on the MUFU); the KL numerator is kept
-            // relative to the slice shift sigma = m_s,l - m_s,l-1 (restored in float64 by the tail)
-            unsigned long long rec[L];
-            Partial pr[L];
+            PROF(2)
             float msl[L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                float ms = wm[l];
-#pragma unroll
-                for (int o = 16; o > 2; o >>= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, o));
-                msl[l] = ms;
-            }
+            for (int l = 0; l < L; ++l) msl[l] = redux_max_nan(wm[l]);
             float Sx[L], Kx[L];
             int ax[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                float f = exp2f_fma((wm[l] - msl[l]) * LOG2E);   // FMA pipe: MUFU is busy
-                if (!(wm[l] > NEG_MASKED)) f = (msl[l] > NEG_MASKED) ? 0.f : 1.f;   // fully masked warp
+                float f = wm[l] == msl[l] ? 1.f : ex2f((wm[l] - msl[l]) * LOG2E);
+                if (!(wm[l] > NEG_MASKED)) f = (act && !(msl[l] > NEG_MASKED)) ? 1.f : 0.f;   // masked warp
                 Sx[l] = Sw[l] * f;
                 Kx[l] = 0.f;
                 if (l > 0 && f != 0.f) {
+                    // KL numerator relative to the slice shift sigma = R_s,l - R_s,l-1
                     const float dsh = (wm[l] - wm[l > 0 ? l - 1 : 0]) - (msl[l] - msl[l > 0 ? l - 1 : 0]);
                     Kx[l] = f * fmaf(dsh, Sw[l], Kw[l]);
                 }
                 ax[l] = (wm[l] == msl[l]) ? aw[l] : 0x7fffffff;
             }
+            PROF(3)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
                     Sx[l] += __shfl_xor_sync(0xffffffffu, Sx[l], o);
                     if (l > 0) Kx[l] += __shfl_xor_sync(0xffffffffu, Kx[l], o);
-                    if (GREEDY) ax[l] = min(ax[l], __shfl_xor_sync(0xffffffffu, ax[l], o));
                 }
             }
+            if (GREEDY) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) ax[l] = redux_min_s32(ax[l]);
+            }
+            PROF(4)
+            // lanes 0..L-1 publish one row each: the Partial, then the self-validating record
+            // (sum != 0: the slice's own reference entry has e = 1 in the sum)
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                rec[l] = ((unsigned long long)__float_as_uint(Sx[l]) << 32) | __float_as_uint(msl[l]);
-                pr[l].m = msl[l];
-                pr[l].amax = ax[l];
-                pr[l].S = f2d_alu(Sx[l]);
-                pr[l].Kl = f2d_alu(Kx[l]);     // relative to the slice shift (see the tail)
-            }
-            // lane 0 issues every record store and then the counter increment with release
-            // semantics, so a fetcher that sees the count complete sees every record
-            if (lane == 0) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
+                if (lane == l) {
                     const size_t idx = ((size_t)u * L + l) * C + s;
-                    p.partials[idx] = pr[l];
-                    st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx, rec[l]);
+                    Partial pr;
+                    pr.m = msl[l];
+                    pr.amax = GREEDY ? ax[l] : 0;
+                    pr.S = f2d_alu(Sx[l]);
+                    pr.Kl = f2d_alu(Kx[l]);
+                    p.partials[idx] = pr;
+                    st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
+                                   ((unsigned long long)__float_as_uint(Sx[l]) << 32) | __float_as_uint(msl[l]));
                 }
-                stamp(j, 5);
             }
+            __syncwarp();
+            if (lane == 0) {
+                stamp(j, 5);
+                mbar_arrive(&c.pub[k]);
+            }
+            PROF(1)
+            PROF_ITEM
         }
+        PROF_FLUSH(2)
     } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
         // ================================================================ fetchers (pass-2 factors)
+        PROF_DECL
         const int f = warp - W_FETCH0;
         const int LC = L * C;     // <= FBUF (checked on the host)
         unsigned long long* fb = c.fbuf[f];
         for (int j = f; j < n_my; j += NFETCH) {
             int64_t u, b, i;
-            int s;
-            item(j, u, s, b, i);
-            const int q = (int)(j % NR);
-            const uint64_t t0 = globaltimer();
+            item(j, u, b, i);
+            const int k = j & (NQ - 1);
             if (lane == 0) stamp(j, 6);
-            if (lane == 0) stamp(j, 7);
+            // the other slices of the unit are published around the time this one is: poll only
+            // from then on (polls steal issue slots and L2 bandwidth)
+            mbar_wait(&c.pub[k], (uint32_t)((j / NQ) & 1));
+            const uint64_t t0 = globaltimer();
+            PROF(4)
             // stage the unit's records; a record whose sum is still 0 is not yet visible
             const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
             while (true) {
@@ -668,101 +882,128 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     }
                     break;
                 }
-                __nanosleep(32);
+                __nanosleep(64);
             }
             __syncwarp();
             if (lane == 0) stamp(j, 4);
-            // row normalisers from the C slice records, all L rows interleaved.  fp32 on the
-            // FMA pipe: the slice sums are fp32-accurate already and FP64 is slow on this part.
-            float Ml[L], Sl[L];
-            {
+            PROF(0)
+            // row normalisers N_l from the C slice records, relative to this slice's own record
+            // reference R_l (fp32).  A slice reference more than 2^127 above R_l, or a masked
+            // own slice, falls back to the maximum reference.
+            float Rl[L], Sl[L];
 #pragma unroll
-                for (int l = 0; l < L; ++l) Ml[l] = -INFINITY;
+            for (int l = 0; l < L; ++l) {
+                Rl[l] = __uint_as_float((uint32_t)fb[l * C + s]);
+                Sl[l] = 0.f;
+            }
+            for (int t = lane; t < C; t += 32) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    const unsigned long long r = fb[l * C + t];
+                    const float vm = __uint_as_float((uint32_t)r);
+                    if (vm > NEG_MASKED)
+                        Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma_any((vm - Rl[l]) * LOG2E), Sl[l]);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) Sl[l] += __shfl_xor_sync(0xffffffffu, Sl[l], o);
+            }
+            bool slow = false;
+#pragma unroll
+            for (int l = 0; l < L; ++l) slow = slow || !(Rl[l] > NEG_MASKED) || !(Sl[l] < INFINITY);
+            if (slow) {
+#pragma unroll
+                for (int l = 0; l < L; ++l) Rl[l] = -INFINITY;
                 for (int t = lane; t < C; t += 32) {
 #pragma unroll
-                    for (int l = 0; l < L; ++l) Ml[l] = fmaxf(Ml[l], __uint_as_float((uint32_t)fb[l * C + t]));
+                    for (int l = 0; l < L; ++l) Rl[l] = fmaxf(Rl[l], __uint_as_float((uint32_t)fb[l * C + t]));
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                    for (int l = 0; l < L; ++l) Ml[l] = fmaxf(Ml[l], __shfl_xor_sync(0xffffffffu, Ml[l], o));
+                for (int l = 0; l < L; ++l) {
+                    Rl[l] = warp_max(Rl[l]);
+                    Sl[l] = 0.f;
                 }
-#pragma unroll
-                for (int l = 0; l < L; ++l) Sl[l] = 0.f;
                 for (int t = lane; t < C; t += 32) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         const unsigned long long r = fb[l * C + t];
                         const float vm = __uint_as_float((uint32_t)r);
                         if (vm > NEG_MASKED)
-                            Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma((vm - Ml[l]) * LOG2E), Sl[l]);
+                            Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma((vm - Rl[l]) * LOG2E), Sl[l]);
                     }
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                    for (int l = 0; l < L; ++l) Sl[l] += __shfl_xor_sync(0xffffffffu, Sl[l], o);
-                }
+                for (int l = 0; l < L; ++l) Sl[l] = warp_sum(Sl[l]);
             }
-            // per-warp factors: lane = 8 (l - 1) + w for pass-1 warp w and the pair ending at row l
-            if (lane == 0) stamp(j, 8);
-            if (j >= NR) mbar_wait(&c.rowf_empty[q], (uint32_t)(((j / NR) - 1) & 1));
-            if (lane == 0) stamp(j, 9);
-            {
-                const int w = lane & 7, l = 1 + (lane >> 3);
-                if (l < L) {
-                    float Ma = Ml[0], Mb = Ml[0], Sa = Sl[0], Sb = Sl[0];
+            PROF(1)
+            if (j >= NQ) mbar_wait(&c.rowf_empty[k], (uint32_t)(((j / NQ) - 1) & 1));
+            PROF(2)
+            // per-region factors: x = NCW (l - 1) + w for region w and the pair ending at row l
+            for (int x = lane; x < (L - 1) * NCW; x += 32) {
+                const int w = x % NCW, l = 1 + x / NCW;
+                if (w < nact) {
+                    float Ma = Rl[0], Mb = Rl[0], Sa = Sl[0], Sb = Sl[0];
 #pragma unroll
                     for (int r = 1; r < L; ++r)
-                        if (r == l) { Ma = Ml[r]; Sa = Sl[r]; Mb = Ml[r - 1]; Sb = Sl[r - 1]; }
-                    const float wa = c.wmx[q][l][w], wb = c.wmx[q][l - 1][w];
-                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? exp2f_fma((wa - Ma) * LOG2E) : 0.f;
-                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp2f_fma((wb - Mb) * LOG2E) : 0.f;
-                    const bool skip = !(ca > 0.f) || !(Sa > 0.f) || !(Sb > 0.f) || !isfinite(Sa) || !isfinite(Sb);
+                        if (r == l) { Ma = Rl[r]; Sa = Sl[r]; Mb = Rl[r - 1]; Sb = Sl[r - 1]; }
+                    const float wa = c.wmx[k][l][w], wb = c.wmx[k][l - 1][w];
+                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? exp2f_fma_any((wa - Ma) * LOG2E) : 0.f;
+                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp2f_fma_any((wb - Mb) * LOG2E) : 0.f;
+                    const bool skip = !(ca > 0.f) || !(Sa > 0.f) || !(Sb > 0.f) || !isfinite(Sa) || !isfinite(Sb) ||
+                                      !isfinite(ca) || !isfinite(cb);
                     WF wf;
                     // identical rows must give rho = 1 exactly (zero residual), which the
                     // Newton reciprocal alone does not guarantee
                     const float num = cb * Sa, den = Sb * ca;
                     wf.rho = skip ? 0.f : (num == den ? 1.f : num * frcp_fma(den));
                     wf.scale = skip ? 0.f : ca * frcp_fma(Sa);
-                    c.rowf[q][l][w] = wf;
+                    c.rowf[k][l][w] = wf;
                 }
             }
             __syncwarp();
             if (lane == 0) {
                 stamp(j, 10);
-                mbar_arrive(&c.rowf_full[q]);
+                mbar_arrive(&c.rowf_full[k]);
             }
+            PROF(3)
+            PROF_ITEM
         }
+        PROF_FLUSH(3)
     } else if (warp == W_RED) {
         // ================================================================ reducer (slice residual)
-        const int w = lane >> 2, t = lane & 3;
+        PROF_DECL
+        const int v = lane >> 2, t = lane & 3;
+        const bool act = v < np2;
         for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
-            int s;
-            item(j, u, s, b, i);
-            const int r2 = (int)(j % R2);
+            item(j, u, b, i);
+            const int r2 = j & (R2 - 1);
             mbar_wait(&c.r2_full[r2], (uint32_t)((j / R2) & 1));
-            if (lane == 0) stamp(j, 14);
+            PROF(0)
             float R[L];
 #pragma unroll
             for (int l = 1; l < L; ++l) {
-                float d = c.r2R[r2][l][w][t] * c.r2scale[r2][l][w];
+                float d = act ? c.r2R[r2][l][v][t] : 0.f;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 R[l] = d;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r2_empty[r2]);
             if (lane >= 1 && lane < L) {
-                float v = R[1];
+                float x = R[1];
 #pragma unroll
                 for (int l = 2; l < L; ++l)
-                    if (lane == l) v = R[l];
-                p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = f2d_alu(v);
+                    if (lane == l) x = R[l];
+                p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = f2d_alu(x);
             }
             if (lane == 0) stamp(j, 15);
+            PROF(1)
+            PROF_ITEM
         }
+        PROF_FLUSH(4)
     }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -771,16 +1012,32 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     if (warp == W_PROD) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(c.taddr));
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
 template <typename Tin, int L, bool G>
 static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     CoreParams p = p0;
     const int ES = (int)sizeof(Tin);
-    const size_t stage_bytes = (size_t)L * VS * ES;
-    const int S = core_stages(L, ES);
+    const int NT = core_tslots(L);
+    const int nact = std::min(NCW, (p.VSe + WCH - 1) / WCH);
+    p.rs = nact * WCH;
+    const size_t ctl = align_up(sizeof(Ctl<L>), 128);
+    const size_t stage_bytes = (size_t)L * p.rs * ES;
+    int S = (int)((SMEM_BUDGET - ctl - 256) / stage_bytes);
+    S = std::min(S, std::min(SMAX, env_int("MSD_STAGES", SMAX)));
+    if (S < 2) return cudaErrorInvalidConfiguration;
     p.stages = S;
-    const int nss = core_sslots(L, ES, (int)sizeof(Ctl<L>));
-    const size_t smem = align_up(stage_bytes * S, 128) + align_up(sizeof(Ctl<L>), 128) +
-                        (size_t)nss * L * CET * CTH * 4 + 128;
+    // item pattern: T items use the NT TMEM slots; R items keep their ring stage.  Of the S
+    // stages ~4 are needed in flight for the TMA; the rest may hold R items.
+    int pt = env_int("MSD_PAT_T", NT), pr = env_int("MSD_PAT_R", -1);
+    if (pr < 0) pr = std::max(0, std::min(NT, S - 5));
+    if (pt < 1) pt = 1;
+    p.pat_t = pt;
+    p.pat_p = pt + pr;
+    const size_t smem = ctl + (size_t)S * stage_bytes + 128;
     auto k = core_kernel<Tin, L, G>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -25,7 +25,9 @@ struct CoreParams {
     uint32_t kinv;      // ceil(2^32 / K): u / K == umulhi(u, kinv) for u < 2^24
     int64_t V;
     int64_t n_items;
-    int32_t stages;
+    int32_t stages;     // TMA ring stages (host-computed from the shared-memory budget)
+    int32_t rs;         // ring row stride in entries (active pass-1 warps x 512)
+    int32_t pat_p, pat_t;   // item pattern: of every pat_p items the first pat_t park e in TMEM
     Partial* partials;
     float2* partms;     // compact (slice max, slice sum) for the pass-2 exchange
     RowStat* rowstat;
