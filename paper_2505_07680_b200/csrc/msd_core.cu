@@ -50,12 +50,13 @@
 namespace msd {
 
 constexpr int NCW = 8;                 // pass-1 warps = element regions of a slice
-constexpr int NCW2 = 4;                // pass-2 warps: warp v handles regions v and v + 4
+constexpr int NCW2 = 8;                // pass-2 warps: warp v handles regions v, v + NCW2, ...
+constexpr int NPR = NCW / NCW2;        // regions per pass-2 warp
 constexpr int CTH = NCW * 32;          // pass-1 threads
 constexpr int CET = VS / CTH;          // elements per pass-1 thread per row (16)
 constexpr int WCH = CET * 32;          // contiguous slice entries per pass-1 warp (512)
 constexpr int TCOLS = 256;             // TMEM columns per region (2 regions per lane quadrant)
-constexpr int NFETCH = 4;
+constexpr int NFETCH = 2;
 // Warp numbering: latency-critical service warps first, then pass 2, then the throughput
 // warps (pass 1).  Pass-1 warp W_P1 + r owns region r in TMEM lane quadrant r % 4; pass-2
 // warp W_P2 + v serves regions v and v + 4 (quadrant v): both bases are multiples of 4.
@@ -63,7 +64,7 @@ constexpr int W_PROD = 0, W_PUB = 1, W_FETCH0 = 2, W_RED = W_FETCH0 + NFETCH;
 constexpr int W_P2 = 8, W_P1 = W_P2 + NCW2;
 constexpr int NG1 = 2;                 // pass-1 warp groups: group g processes items j = g mod NG1
 constexpr int CORE_THREADS = (W_P1 + NG1 * NCW) * 32;
-static_assert(W_RED < W_P2 && W_P2 % 4 == 0 && W_P1 % 4 == 0 && NCW == 2 * NCW2, "warp roles");
+static_assert(W_RED < W_P2 && W_P2 % 4 == 0 && W_P1 % 4 == 0 && NCW % NCW2 == 0 && NCW2 % 4 == 0, "warp roles");
 constexpr int SMAX = 14;               // ring stages (upper bound)
 constexpr int NQ = 16;                 // per-item record slots (references, pass-2 factors)
 constexpr int NTMAX = 8;               // TMEM item slots (upper bound)
@@ -87,8 +88,8 @@ struct Ctl {
     uint32_t taddr;
     float wmx[NQ][L][NCW];                  // per-warp max of each row, per item
     uint32_t clampw[NQ];                    // bit w: pass-1 warp w took the clamped path
-    float r1S[R1][L][NCW][NSUB];            // pass-1 partial sums
-    float r1K[R1][L][NCW][NSUB];            // pass-1 KL numerators (relative to the warp shift)
+    alignas(16) float r1S[R1][L][NCW][NSUB];   // pass-1 partial sums
+    alignas(16) float r1K[R1][L][NCW][NSUB];   // pass-1 KL numerators (relative to the warp shift)
     int r1A[R1][L][NCW];                    // greedy: first argmax index per warp
     WF rowf[NQ][L][NCW];
     float r2R[R2][L][NCW2][NSUB];           // pass-2 residual partials (probability units)
@@ -310,7 +311,7 @@ __device__ __forceinline__ void tm_st8(uint32_t ta, const float* v) {
 #define PROF_DECL long long _pa[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long _pt = clock64(); long long _pn = 0;
 #define PROF(k) { const long long _t = clock64(); _pa[k] += _t - _pt; _pt = _t; }
 #define PROF_ITEM ++_pn;
-#define PROF_FLUSH(role) if (p.trace && lane == 0) { for (int _k = 0; _k < 8; ++_k) atomicAdd(p.trace + (role) * 16 + _k, (unsigned long long)_pa[_k]); atomicAdd(p.trace + (role) * 16 + 15, (unsigned long long)_pn); }
+#define PROF_FLUSH(role) if (p.trace && lane == 0) { for (int _k = 0; _k < 8; ++_k) { atomicAdd(p.trace + (role) * 16 + _k, (unsigned long long)_pa[_k]); atomicAdd(p.trace + 128 + ((size_t)blockIdx.x * 8 + (role)) * 16 + _k, (unsigned long long)_pa[_k]); } atomicAdd(p.trace + (role) * 16 + 15, (unsigned long long)_pn); atomicAdd(p.trace + 128 + ((size_t)blockIdx.x * 8 + (role)) * 16 + 15, (unsigned long long)_pn); }
 #else
 #define PROF_DECL
 #define PROF(k)
@@ -362,14 +363,21 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     const int grp = blockIdx.x / C, sfix = blockIdx.x % C;
     const int n_my = grp < kgrp && grp < p.U ? (p.U - grp + kgrp - 1) / kgrp : 0;
 
-    // the ring tail [VSe, RS) of every row is never written by the bulk copies: the pad value
-    // once, so that the last active warp loads whole vectors unconditionally
+    // this CTA's slice s = blockIdx % C is the same for all its items, so is its length: the
+    // ring tail [len_bulk, RS) of every row is never written by the bulk copies -- the pad
+    // value (~ -2.4e30) once, so every active warp loads whole vectors unconditionally (and the
+    // last slice of a row needs no second copy)
+    const int s = sfix;
+    const int64_t base = (int64_t)s * VSe;
+    const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
+    const int len_bulk = (len * ES) / 16 * 16 / ES;
     {
         uint32_t* r32 = reinterpret_cast<uint32_t*>(ring);
-        const int per_row = (RS - VSe) * ES / 4;
+        const int w0 = len_bulk * ES / 4;
+        const int per_row = RS * ES / 4 - w0;
         for (int e = tid; e < S * L * per_row; e += blockDim.x) {
             const int row = e / per_row;
-            r32[(size_t)row * (RS * ES / 4) + VSe * ES / 4 + (e - row * per_row)] = 0xF1F1F1F1u;
+            r32[(size_t)row * (RS * ES / 4) + w0 + (e - row * per_row)] = 0xF1F1F1F1u;
         }
     }
     if (warp == W_PROD) {
@@ -409,10 +417,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     };
     // TMEM column base of region w (lane quadrant w & 3, column block w >> 2)
     auto tcol = [&](int w) { return c.taddr + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((w >> 2) * TCOLS); };
-    const int s = sfix;
-    const int64_t base = (int64_t)s * VSe;
-    const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
-    const int len_bulk = (len * ES) / 16 * 16 / ES;
 
     const bool p1only = (p.dbg & 1) != 0;   // debug: pass 1 + TMA ring only (results invalid)
     if (p1only && warp != W_PROD && warp < W_P1) {
@@ -600,11 +604,13 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
     } else if (warp >= W_P2) {
         // ================================================================ pass-2 warps
-        // warp W_P2 + v handles regions v and v + NCW2 (same TMEM lane quadrant)
+        // warp W_P2 + v handles regions v, v + NCW2, ... (same TMEM lane quadrant)
         const int v = warp - W_P2;
         if (v < np2) {
             PROF_DECL
-            const bool two = v + NCW2 < nact;
+            int nreg = 0;        // active regions of this warp
+#pragma unroll
+            for (int h = 0; h < NPR; ++h) nreg += (v + h * NCW2 < nact) ? 1 : 0;
             Cursor cu;
             for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
                 const int j = cu.j;
@@ -614,16 +620,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int r2 = j & (R2 - 1);
                 mbar_wait(&c.rowf_full[k], (uint32_t)((j / NQ) & 1));
                 PROF(0)
-                float rh[2][L], sc[2][L], wm[2][L];
+                float rh[NPR][L], sc[NPR][L], wm[NPR][L];
                 const uint32_t cw = c.clampw[k];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < NPR; ++h) {
                     const int w = v + h * NCW2;
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         rh[h][l] = sc[h][l] = 0.f;
                         wm[h][l] = 0.f;
-                        if (h == 0 || two) {
+                        if (h < nreg) {
                             if (l > 0) {
                                 rh[h][l] = c.rowf[k][l][w].rho;
                                 sc[h][l] = c.rowf[k][l][w].scale;
@@ -658,18 +664,23 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     PROF(1)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (h == 0 || two) {
+                    for (int h = 0; h < NPR; ++h) {
+                        if (h < nreg) {
                             const uint32_t tb = tcol(v + h * NCW2) + (uint32_t)(q * CET * L);
-                            float ea[CET], eb[CET];
+                            float ea[CET], eb[CET], ec[CET];
                             tm_ld16(tb, eb);
+                            tm_ld16(tb + (uint32_t)CET, ea);
+                            if (L > 2) tm_ld16(tb + (uint32_t)(2 * CET), ec);
+                            tm_wait_ld();
+                            pair(h, 1, ea, eb);
+                            if (L > 2) pair(h, 2, ec, ea);
 #pragma unroll
-                            for (int l = 1; l < L; ++l) {
-                                tm_ld16(tb + (uint32_t)(l * CET), ea);
+                            for (int l = 3; l < L; ++l) {
+#pragma unroll
+                                for (int kk = 0; kk < CET; ++kk) eb[kk] = ec[kk];
+                                tm_ld16(tb + (uint32_t)(l * CET), ec);
                                 tm_wait_ld();
-                                pair(h, l, ea, eb);
-#pragma unroll
-                                for (int kk = 0; kk < CET; ++kk) eb[kk] = ea[kk];
+                                pair(h, l, ec, eb);
                             }
                         }
                     }
@@ -685,8 +696,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     PROF(1)
                     const Tin* stage = ring + (size_t)cu.st * L * RS;
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (h == 0 || two) {
+                    for (int h = 0; h < NPR; ++h) {
+                        if (h < nreg) {
                             const int w = v + h * NCW2;
                             const bool clamp = ((cw >> w) & 1u) || ES == 4;
                             float eprev[CET];
@@ -706,7 +717,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         }
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cnt(&c.empty[cu.st], two ? 2u : 1u);
+                    if (lane == 0) mbar_arrive_cnt(&c.empty[cu.st], (uint32_t)nreg);
                     PROF(2)
                 }
 #pragma unroll
@@ -730,10 +741,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         PROF_DECL
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            const uint32_t bytes = (uint32_t)((len * ES) / 16 * 16);
-            // the last slice of a row: pad [bulk end, VSe) from the constant pad buffer so
-            // the pass-1 loads stay unconditional (the copy engine does the fill)
-            const uint32_t pad = (uint32_t)(VSe * ES) - bytes;
+            const uint32_t bytes = (uint32_t)(len_bulk * ES);   // [len_bulk, RS) holds the pad
             Cursor cu;
             for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
                 const int j = cu.j;
@@ -742,15 +750,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 int64_t u, b, i;
                 item(j, u, b, i);
                 stamp(j, 0);
-                mbar_arrive_expect_tx(&c.full[cu.st], (bytes + pad) * L);
+                if (bytes) {
+                    mbar_arrive_expect_tx(&c.full[cu.st], bytes * L);
 #pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    Tin* dst = ring + ((size_t)cu.st * L + l) * RS;
-                    if (bytes) {
+                    for (int l = 0; l < L; ++l) {
+                        Tin* dst = ring + ((size_t)cu.st * L + l) * RS;
                         const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] + i * p.lv.ld[l] + base;
                         bulk_g2s(dst, src, bytes, &c.full[cu.st], pol);
                     }
-                    if (pad) bulk_g2s(reinterpret_cast<unsigned char*>(dst) + bytes, p.pad, pad, &c.full[cu.st], pol);
+                } else {
+                    mbar_arrive(&c.full[cu.st]);   // nothing to copy (a slice past the row end)
                 }
                 PROF(1)
                 PROF_ITEM
@@ -759,11 +768,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         PROF_FLUSH(5)
     } else if (warp == W_PUB) {
         // ================================================================ publisher
-        // lane = 4 w + t: region w, sub-record t.  Factors 2^((R_w - R_s) log2 e) relative to the
-        // largest reference R_s (all 1 when every warp used the slice reference).
+        // lane = 8 l + w: row l, region w (L <= 4).  Each lane sums its region's sub-records,
+        // scales them by 2^((m_w - m_s) log2 e) relative to the slice maximum m_s (1 when the
+        // region holds the maximum) and the row's 8 lanes reduce with 3 shuffle levels.
+        static_assert(NCW == 8 && L * NCW <= 32, "publisher lane layout");
         PROF_DECL
-        const int w = lane >> 2, t = lane & 3;
-        const bool act = w < nact;
+        const int l = lane >> 3, w = lane & 7;
+        const bool inrow = l < L;
+        const bool act = inrow && w < nact;
         for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             item(j, u, b, i);
@@ -771,65 +783,55 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int r1 = j & (R1 - 1);
             mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
             PROF(0)
-            float Sw[L], Kw[L], wm[L];
-            int aw[L];
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                Sw[l] = act ? c.r1S[r1][l][w][t] : 0.f;
-                Kw[l] = act ? c.r1K[r1][l][w][t] : 0.f;
-                wm[l] = act ? c.wmx[k][l][w] : -INFINITY;
-                aw[l] = (GREEDY && act && t == 0) ? c.r1A[r1][l][w] : 0x7fffffff;
+            float Sw = 0.f, Kw = 0.f, wm = -INFINITY, wmp = -INFINITY;
+            int aw = 0x7fffffff;
+            if (act) {
+                const float4 s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
+                const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][w][0]);
+                Sw = (s4.x + s4.y) + (s4.z + s4.w);
+                Kw = (k4.x + k4.y) + (k4.z + k4.w);
+                wm = c.wmx[k][l][w];
+                wmp = c.wmx[k][l > 0 ? l - 1 : 0][w];
+                if (GREEDY) aw = c.r1A[r1][l][w];
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
             PROF(2)
-            float msl[L];
+            // slice maximum of the row (NaN-propagating) over the row's 8 lanes
+            float msl = wm;
 #pragma unroll
-            for (int l = 0; l < L; ++l) msl[l] = redux_max_nan(wm[l]);
-            float Sx[L], Kx[L];
-            int ax[L];
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                float f = wm[l] == msl[l] ? 1.f : ex2f((wm[l] - msl[l]) * LOG2E);
-                if (!(wm[l] > NEG_MASKED)) f = (act && !(msl[l] > NEG_MASKED)) ? 1.f : 0.f;   // masked warp
-                Sx[l] = Sw[l] * f;
-                Kx[l] = 0.f;
-                if (l > 0 && f != 0.f) {
-                    // KL numerator relative to the slice shift sigma = R_s,l - R_s,l-1
-                    const float dsh = (wm[l] - wm[l > 0 ? l - 1 : 0]) - (msl[l] - msl[l > 0 ? l - 1 : 0]);
-                    Kx[l] = f * fmaf(dsh, Sw[l], Kw[l]);
-                }
-                ax[l] = (wm[l] == msl[l]) ? aw[l] : 0x7fffffff;
+            for (int o = 4; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
+            const float mslp = __shfl_sync(0xffffffffu, msl, (lane - 8) & 31);   // previous row's
+            float f = wm == msl ? 1.f : ex2f((wm - msl) * LOG2E);
+            if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
+            float Sx = Sw * f, Kx = 0.f;
+            if (l > 0 && f != 0.f) {
+                // KL numerator relative to the slice shift sigma = m_s,l - m_s,l-1
+                const float dsh = (wm - wmp) - (msl - mslp);
+                Kx = f * fmaf(dsh, Sw, Kw);
             }
+            int ax = (wm == msl) ? aw : 0x7fffffff;
             PROF(3)
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    Sx[l] += __shfl_xor_sync(0xffffffffu, Sx[l], o);
-                    if (l > 0) Kx[l] += __shfl_xor_sync(0xffffffffu, Kx[l], o);
-                }
-            }
-            if (GREEDY) {
-#pragma unroll
-                for (int l = 0; l < L; ++l) ax[l] = redux_min_s32(ax[l]);
+            for (int o = 4; o > 0; o >>= 1) {
+                Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
+                Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
+                if (GREEDY) ax = min(ax, __shfl_xor_sync(0xffffffffu, ax, o));
             }
             PROF(4)
-            // lanes 0..L-1 publish one row each: the Partial, then the self-validating record
-            // (sum != 0: the slice's own reference entry has e = 1 in the sum)
-#pragma unroll
-            for (int l = 0; l < L; ++l) {
-                if (lane == l) {
-                    const size_t idx = ((size_t)u * L + l) * C + s;
-                    Partial pr;
-                    pr.m = msl[l];
-                    pr.amax = GREEDY ? ax[l] : 0;
-                    pr.S = f2d_alu(Sx[l]);
-                    pr.Kl = f2d_alu(Kx[l]);
-                    p.partials[idx] = pr;
-                    st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
-                                   ((unsigned long long)__float_as_uint(Sx[l]) << 32) | __float_as_uint(msl[l]));
-                }
+            // lane 8 l publishes row l: first the self-validating exchange record (the other
+            // slices wait for it; sum != 0: the slice maximum's entry has e = 1 in the sum),
+            // then the Partial for the tail
+            if (inrow && w == 0) {
+                const size_t idx = ((size_t)u * L + l) * C + s;
+                st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
+                               ((unsigned long long)__float_as_uint(Sx) << 32) | __float_as_uint(msl));
+                Partial pr;
+                pr.m = msl;
+                pr.amax = GREEDY ? ax : 0;
+                pr.S = f2d_alu(Sx);
+                pr.Kl = f2d_alu(Kx);
+                p.partials[idx] = pr;
             }
             __syncwarp();
             if (lane == 0) {
@@ -902,7 +904,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const unsigned long long r = fb[l * C + t];
                     const float vm = __uint_as_float((uint32_t)r);
                     if (vm > NEG_MASKED)
-                        Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma_any((vm - Rl[l]) * LOG2E), Sl[l]);
+                        Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), ex2f((vm - Rl[l]) * LOG2E), Sl[l]);
                 }
             }
 #pragma unroll
@@ -949,16 +951,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     for (int r = 1; r < L; ++r)
                         if (r == l) { Ma = Rl[r]; Sa = Sl[r]; Mb = Rl[r - 1]; Sb = Sl[r - 1]; }
                     const float wa = c.wmx[k][l][w], wb = c.wmx[k][l - 1][w];
-                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? exp2f_fma_any((wa - Ma) * LOG2E) : 0.f;
-                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? exp2f_fma_any((wb - Mb) * LOG2E) : 0.f;
+                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? ex2f((wa - Ma) * LOG2E) : 0.f;
+                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? ex2f((wb - Mb) * LOG2E) : 0.f;
                     const bool skip = !(ca > 0.f) || !(Sa > 0.f) || !(Sb > 0.f) || !isfinite(Sa) || !isfinite(Sb) ||
                                       !isfinite(ca) || !isfinite(cb);
                     WF wf;
                     // identical rows must give rho = 1 exactly (zero residual), which the
                     // Newton reciprocal alone does not guarantee
                     const float num = cb * Sa, den = Sb * ca;
-                    wf.rho = skip ? 0.f : (num == den ? 1.f : num * frcp_fma(den));
-                    wf.scale = skip ? 0.f : ca * frcp_fma(Sa);
+                    wf.rho = skip ? 0.f : (num == den ? 1.f : __fdiv_rn(num, den));
+                    wf.scale = skip ? 0.f : __fdiv_rn(ca, Sa);
                     c.rowf[k][l][w] = wf;
                 }
             }
@@ -987,7 +989,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             for (int l = 1; l < L; ++l) {
                 float d = act ? c.r2R[r2][l][v][t] : 0.f;
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                for (int o = NCW2 * NSUB / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 R[l] = d;
             }
             __syncwarp();

@@ -35,3 +35,16 @@ for r, (rn, ph) in roles.items():
         continue
     v = a[r, :len(ph)] / n
     print(f"  {rn:9s} items {int(n):7d}  " + "  ".join(f"{p} {x:.0f}" for p, x in zip(ph, v.tolist())) + f"  | total {v.sum():.0f} cyc/item")
+
+# per-CTA view: the CTAs whose pass-1 warps waited least for slots pace their group
+G = 148
+pc = buf[128:128 + G * 8 * 16].view(G, 8, 16).cpu().double()
+n1 = pc[:, 0, 15].clamp(min=1)
+slots = pc[:, 0, 1] / n1
+full = pc[:, 0, 0] / n1
+order = torch.argsort(slots)
+print("per-CTA pass-1 cycles/item (fewest slot waits first):")
+for g in order[:6].tolist() + order[-3:].tolist():
+    v = pc[g, 0, :6] / n1[g]
+    w = pc[g, 1, :5] / pc[g, 1, 15].clamp(min=1)
+    print(f"  cta {g:3d}: p1 " + " ".join(f"{x:.0f}" for x in v.tolist()) + " | p2 " + " ".join(f"{x:.0f}" for x in w.tolist()))

@@ -58,3 +58,32 @@ lastx = np.array([np.nanmax(t[cta == g]) for g in range(G)])
 print("CTA first-issue us: min %.1f med %.1f max %.1f" % (first.min(), np.median(first), first.max()))
 print("CTA last-stamp  us: min %.1f med %.1f max %.1f" % (lastx.min(), np.median(lastx), lastx.max()))
 print("slowest CTAs:", np.argsort(-lastx)[:8].tolist(), "earliest-finishing:", np.argsort(lastx)[:8].tolist())
+# --- who publishes last, and why: per unit, the last publisher's phase times vs the others'
+last_c = np.nanargmax(pub, 1)
+T = t.reshape(U, C, 16)
+uu = np.arange(U)
+lastT = T[uu, last_c]                       # (U, 16) stamps of the last publisher
+def med(x): return np.nanmedian(x)
+print("last publisher: slot wait (p1.full->p1.tmE) med %.2f, p1 compute (tmE->end) %.2f, tma->full %.2f, end->pub %.2f"
+      % (med(lastT[:, 2] - lastT[:, 1]), med(lastT[:, 3] - lastT[:, 2]), med(lastT[:, 1] - lastT[:, 0]), med(lastT[:, 5] - lastT[:, 3])))
+print("all CTAs:       slot wait med %.2f, p1 compute %.2f, tma->full %.2f, end->pub %.2f"
+      % (med(T[:, :, 2] - T[:, :, 1]), med(T[:, :, 3] - T[:, :, 2]), med(T[:, :, 1] - T[:, :, 0]), med(T[:, :, 5] - T[:, :, 3])))
+# is the last publisher of unit u also late on u-k?  (persistence of slowness)
+lc = last_c.reshape(-1)
+for lag in (kg, 2 * kg, 4 * kg):
+    same = np.mean(lc[lag:] == lc[:-lag])
+    print(f"P(last publisher of unit u == of unit u-{lag}) = {same:.2f}  (chance {1 / C:.3f})")
+print("last-publisher slice histogram (top):", np.bincount(lc, minlength=C).argsort()[::-1][:8].tolist())
+# --- timeline of the most frequent last publisher (per group) vs a typical CTA
+cta_of_last = (uu % kg) * C + lc
+for g in range(min(kg, 2)):
+    sel_units = (uu % kg) == g
+    vals, cnts = np.unique(cta_of_last[sel_units], return_counts=True)
+    straggler = int(vals[np.argmax(cnts)])
+    for name, cta_id in (("straggler", straggler), ("typical", g * C + (straggler % C + 7) % C)):
+        Tc = t[cta == cta_id]
+        seg = lambda a, b: np.nanmedian(Tc[:, b] - Tc[:, a])
+        gap = np.nanmedian(np.diff(Tc[:, 1]))
+        print(f"group {g} {name:9s} cta {cta_id:3d}: period {gap:.2f}  tma->full {seg(0,1):.2f} slot {seg(1,2):.2f} "
+              f"p1 {seg(2,3):.2f} end->pub {seg(3,5):.2f} pub->seen {seg(5,4):.2f} combine {seg(4,10):.2f} "
+              f"->p2 {seg(10,12):.2f} p2 {seg(12,13):.2f} | p1.end->p2 {seg(3,12):.2f}")
