@@ -338,20 +338,20 @@ __device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out
                                       const Partial* prev = nullptr) {
     const int lane = threadIdx.x & 31;
     float m = -INFINITY;
-    for (int s = lane; s < C; s += 32) m = fmaxf(m, __ldcg(&parts[s].m));
+    for (int s = lane; s < C; s += 32) m = fmaxf(m, parts[s].m);
     m = warp_max(m);
     double S = 0.0, Kl = 0.0;
     int am = 0x7fffffff;
     bool bad = false;
     for (int s = lane; s < C; s += 32) {
-        float ms = __ldcg(&parts[s].m);
-        double Ss = __ldcg(&parts[s].S);
-        double Ks = __ldcg(&parts[s].Kl);
-        double f = exp((double)ms - (double)m);
+        float ms = parts[s].m;
+        double Ss = parts[s].S;
+        double Ks = parts[s].Kl;
+        double f = dexp_neg((double)ms - (double)m);
         S += Ss * f;
-        if (prev) Ks += ((double)ms - (double)__ldcg(&prev[s].m)) * Ss;
+        if (prev) Ks += ((double)ms - (double)prev[s].m) * Ss;
         Kl += Ks * f;
-        if (ms == m) am = min(am, __ldcg(&parts[s].amax));
+        if (ms == m) am = min(am, parts[s].amax);
         if (isnan(ms) || isnan(Ss)) bad = true;
     }
     S = warp_sum_d(S);

@@ -71,6 +71,7 @@ struct TailParams {
     uint32_t* cnt;
     double z_safe;
     int32_t exact_all;
+    int32_t prefetch;   // set by launch_tail: partials + residuals of a request fit in shared memory
 };
 
 struct RollbackParams {

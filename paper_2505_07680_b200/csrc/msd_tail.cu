@@ -20,7 +20,19 @@
 namespace msd {
 
 constexpr int MAXSLICES = 128;   // V <= 524288
+
+#ifdef MSD_PROF
+__device__ unsigned long long g_tail_prof[16];
+__device__ unsigned long long g_tail_cta[4096][2];   // per request: start / end globaltimer
+__device__ unsigned long long g_tail_req[4096][16];  // per request: cycles per phase
+#define TPROF_DECL long long _tp = clock64();
+#define TPROF(k) if (threadIdx.x == 0) { const long long _t = clock64(); atomicAdd(&g_tail_prof[k], (unsigned long long)(_t - _tp)); if (blockIdx.x < 4096) g_tail_req[blockIdx.x][k] += (unsigned long long)(_t - _tp); _tp = _t; }
+#else
+#define TPROF_DECL
+#define TPROF(k)
+#endif
 constexpr double TIE_EPS = 1e-6;
+constexpr double DRAW_MARGIN = 2e-5;   // fp32 draw weights: decide only crossings this far (x Z) from a boundary
 
 struct TailShared {
     RowStat row[MAXC][MAXL];      // row statistics of draft positions i < K (from the core partials)
@@ -42,7 +54,9 @@ struct TailShared {
     int32_t exact;
     double sel_before;
     int32_t sel_slice;
+    float zpre[MAXL][MAXC];       // z_l[b, i, x_i]: the draft token's logit in every row i < K
 };
+constexpr size_t TAIL_DYN_MAX = 96 * 1024;   // prefetched partials + slice residuals
 
 template <typename Tin>
 __device__ __forceinline__ const Tin* row_ptr(const TailParams& p, int l, int64_t b, int64_t i) {
@@ -105,48 +119,150 @@ __device__ __forceinline__ void load_slice(const Tin* row, int64_t V, int s, int
     }
 }
 
-// Row statistics of an arbitrary row (bonus rows at positions >= K): per-slice
-// partials into sh.part[], combined RowStat returned to every thread.
+// One vector (VEC entries) of a row at entry e (a multiple of VEC), clamped; entries >= Vend
+// are NEG_CLAMP.
 template <typename Tin>
-__device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShared& sh) {
+__device__ __forceinline__ void load_vec(const Tin* row, int64_t e, int64_t Vend, float* x) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    if (e + VEC <= Vend) {
+        unpack_clamped<Tin>(__ldg(reinterpret_cast<const uint4*>(row + e)), x);
+    } else {
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) x[k] = (e + k < Vend) ? clamp1(Elem<Tin>::load1(row + e + k)) : NEG_CLAMP;
+    }
+}
+
+// Row statistics of an arbitrary row (bonus rows at positions >= K): per-slice partials into
+// sh.part[] (one warp per slice, online max / sum with float64 accumulation, no block
+// barriers inside), combined RowStat returned to every thread.
+// Fast per-slice partial of a bf16 row for one warp: pass 1 the slice maximum (bf16x2 max
+// tree, redux), pass 2 (L1-resident re-read) sum 2^((z - m) log2 e) with the mixed-precision
+// add.f32.bf16, packed fp32 per vector and float64 across vectors.  Returns false (the caller
+// takes the generic path) when the maximum is not finite.  Argmax only when `want_am`.
+__device__ bool slice_partial_bf16(const __nv_bfloat16* row, int64_t s0, int64_t s1, bool want_am, Partial* out) {
+    const int lane = threadIdx.x & 31;
+    constexpr int VEC = 8, U = 4;   // vectors in flight per lane
+    uint32_t mx = 0xFF80FF80u;   // -inf pair
+    for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
+        uint4 v[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int64_t e = e0 + (int64_t)uu * 32 * VEC;
+            v[uu] = e + VEC <= s1 ? __ldg(reinterpret_cast<const uint4*>(row + e)) : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+            if (e < s1 && e + VEC > s1) {     // straddling vector: element-wise, -inf past the end
+                __nv_bfloat16 xs[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) xs[k] = e + k < s1 ? row[e + k] : __float2bfloat16(-INFINITY);
+                v[uu] = *reinterpret_cast<const uint4*>(xs);
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu)
+            mx = max_nan_bf16x2(mx, max_nan_bf16x2(max_nan_bf16x2(v[uu].x, v[uu].y), max_nan_bf16x2(v[uu].z, v[uu].w)));
+    }
+    float m = fmaxf(bf16lo(mx), bf16hi(mx));
+    if (isnan(bf16lo(mx)) || isnan(bf16hi(mx))) m = NAN;
+    m = warp_max(m);
+    m = __shfl_sync(0xffffffffu, m, 0);
+    if (!(m > NEG_MASKED) || !(m < INFINITY)) return false;
+    const float nm = -m;
+    const float2 l2e = make_float2(LOG2E, LOG2E);
+    double S = 0.0;
+    int am = 0x7fffffff;
+    for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
+        uint4 v[U];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+            const int64_t e = e0 + (int64_t)uu * 32 * VEC;
+            v[uu] = e + VEC <= s1 ? __ldg(reinterpret_cast<const uint4*>(row + e)) : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+            if (e < s1 && e + VEC > s1) {
+                __nv_bfloat16 xs[VEC];
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) xs[k] = e + k < s1 ? row[e + k] : __float2bfloat16(-INFINITY);
+                v[uu] = *reinterpret_cast<const uint4*>(xs);
+            }
+        }
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t w = k == 0 ? v[uu].x : k == 1 ? v[uu].y : k == 2 ? v[uu].z : v[uu].w;
+                float y0, y1;
+                asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.bf16 %0, lo, %3; add.rn.f32.bf16 %1, hi, %3; }"
+                    : "=f"(y0), "=f"(y1) : "r"(w), "f"(nm));
+                const float2 t = __fmul2_rn(make_float2(y0, y1), l2e);
+                acc = __fadd2_rn(acc, make_float2(ex2f(t.x), ex2f(t.y)));
+                if (want_am) {
+                    const int64_t e = e0 + (int64_t)uu * 32 * VEC + 2 * k;
+                    if (y0 == 0.f && am == 0x7fffffff) am = (int)e;
+                    if (y1 == 0.f && am == 0x7fffffff) am = (int)(e + 1);
+                }
+            }
+        }
+        S += (double)(acc.x + acc.y);
+    }
+    S = warp_sum_d(S);
+    if (want_am) am = warp_min_i(am);
+    out->m = m;
+    out->amax = am;
+    out->S = S;
+    out->Kl = 0.0;
+    return true;
+}
+
+template <typename Tin>
+__device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShared& sh, bool want_am = true) {
     constexpr int VEC = Elem<Tin>::VEC;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ float wmx[NWARP], wsm[NWARP];
-    __shared__ int wam[NWARP];
-    for (int s = 0; s < C; ++s) {
-        float x[ET];
-        load_slice<Tin>(row, V, s, vse, x);
-        float tm = x[0];
-#pragma unroll
-        for (int k = 1; k < ET; ++k) tm = fmaxf(tm, x[k]);
-        const float wm = warp_max(tm);
-        float sum = 0.f;
-#pragma unroll
-        for (int k = 0; k < ET; ++k) sum += ex2f((x[k] - wm) * LOG2E);
-        sum = warp_sum(sum);
-        int am = 0x7fffffff;
-#pragma unroll
-        for (int k = ET - 1; k >= 0; --k)
-            if (x[k] == wm) am = (int)((int64_t)s * vse + ((k / VEC) * T + threadIdx.x) * VEC + (k % VEC));
-        am = warp_min_i(am);
-        __syncthreads();
-        if (lane == 0) { wmx[warp] = wm; wsm[warp] = sum; wam[warp] = am; }
-        __syncthreads();
-        if (warp == 0) {
-            const bool act = lane < NWARP;
-            const float mw = act ? wmx[lane] : -INFINITY;
-            const float ms = warp_max(mw);
-            double f = act ? exp((double)mw - (double)ms) : 0.0;
-            if (act && !(mw > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;
-            double Ss = act ? (double)wsm[lane] * f : 0.0;
-            int a = (act && mw == ms) ? wam[lane] : 0x7fffffff;
-            Ss = warp_sum_d(Ss);
-            a = warp_min_i(a);
-            if (lane == 0) {
-                Partial pr;
-                pr.m = ms; pr.amax = a; pr.S = Ss; pr.Kl = 0.0;
-                sh.part[s] = pr;
+    for (int s = warp; s < C; s += NWARP) {
+        if (sizeof(Tin) == 2) {
+            Partial pr;
+            const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
+            if (slice_partial_bf16(reinterpret_cast<const __nv_bfloat16*>(row), s0, s1, want_am, &pr)) {
+                if (lane == 0) sh.part[s] = pr;
+                continue;
             }
+        }
+        const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
+        float m = -INFINITY;
+        double S = 0.0;
+        int am = 0x7fffffff;
+        constexpr int U = 4;    // vectors in flight per lane
+        for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
+            float x[U][VEC];
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) load_vec<Tin>(row, e0 + (int64_t)uu * 32 * VEC, s1, x[uu]);
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                const int64_t e = e0 + (int64_t)uu * 32 * VEC;
+                float mv = x[uu][0];
+#pragma unroll
+                for (int k = 1; k < VEC; ++k) mv = fmaxf(mv, x[uu][k]);
+                if (mv > m) {      // new running maximum: rescale (first index of the maximum kept)
+                    S *= dexp_neg((double)m - (double)mv);
+                    m = mv;
+                    am = 0x7fffffff;
+                }
+                float sv = 0.f;
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) sv += ex2f((x[uu][k] - m) * LOG2E);
+                S += (double)sv;
+#pragma unroll
+                for (int k = 0; k < VEC; ++k)
+                    if (x[uu][k] == m && am == 0x7fffffff && e + k < s1) am = (int)(e + k);
+            }
+        }
+        // combine the lanes (fixed order)
+        const float ms = warp_max(m);
+        double f = dexp_neg((double)m - (double)ms);
+        if (!(m > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;
+        double Ss = warp_sum_d(S * f);
+        const int a = warp_min_i(m == ms ? am : 0x7fffffff);
+        if (lane == 0) {
+            Partial pr;
+            pr.m = ms; pr.amax = a; pr.S = Ss; pr.Kl = 0.0;
+            sh.part[s] = pr;
         }
     }
     __syncthreads();
@@ -160,7 +276,7 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShar
         int am = 0x7fffffff;
         bool bad = false;
         for (int s = lane; s < C; s += 32) {
-            S += sh.part[s].S * exp((double)sh.part[s].m - (double)m);
+            S += sh.part[s].S * dexp_neg((double)sh.part[s].m - (double)m);
             if (sh.part[s].m == m) am = min(am, sh.part[s].amax);
             if (isnan(sh.part[s].m) || isnan(sh.part[s].S)) bad = true;
         }
@@ -181,39 +297,70 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShar
     return r;
 }
 
-// Per-slice residual mass R_s = sum max(p - q, 0) of an arbitrary row pair into
-// sh.w[] (fp32 per element, float64 across warps; the core's pass-2 arithmetic).
+// Per-slice residual mass R_s = sum max(p - q, 0) of an arbitrary row pair into sh.w[]
+// (one warp per slice; fp32 per vector, float64 across vectors and lanes).
 template <typename Tin>
 __device__ void pair_resid(const Tin* ra, const Tin* rb, const RowStat& A, const RowStat& Bq,
                            int64_t V, int C, int vse, TailShared& sh) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const double rho = Bq.S > 0 ? A.S / Bq.S : 0.0;
     const float rh = (float)rho, rl = (float)(rho - (double)rh);
     const float Ma = (float)A.M, Mb = (float)Bq.M;
-    for (int s = 0; s < C; ++s) {
-        float xa[ET], xb[ET];
-        load_slice<Tin>(ra, V, s, vse, xa);
-        load_slice<Tin>(rb, V, s, vse, xb);
-        float acc = 0.f;
+    for (int s = warp; s < C; s += NWARP) {
+        const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
+        double acc = 0.0;
+        constexpr int U = 2;    // vector pairs in flight per lane
+        for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
+            float xa[U][VEC], xb[U][VEC];
 #pragma unroll
-        for (int k = 0; k < ET; ++k) {
-            const float ea = ex2f((xa[k] - Ma) * LOG2E);
-            const float eb = ex2f((xb[k] - Mb) * LOG2E);
-            float t = fmaf(-eb, rh, ea);
-            t = fmaf(-eb, rl, t);
-            acc += fmaxf(t, 0.f);
+            for (int uu = 0; uu < U; ++uu) {
+                load_vec<Tin>(ra, e0 + (int64_t)uu * 32 * VEC, s1, xa[uu]);
+                load_vec<Tin>(rb, e0 + (int64_t)uu * 32 * VEC, s1, xb[uu]);
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+                float av = 0.f;
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) {
+                    const float ea = ex2f((xa[uu][k] - Ma) * LOG2E);
+                    const float eb = ex2f((xb[uu][k] - Mb) * LOG2E);
+                    float t = fmaf(-eb, rh, ea);
+                    t = fmaf(-eb, rl, t);
+                    av += fmaxf(t, 0.f);
+                }
+                acc += (double)av;
+            }
         }
-        const double tot = block_sum_d((double)acc, sh);
-        if (threadIdx.x == 0) sh.w[s] = tot / A.S;
+        acc = warp_sum_d(acc);
+        if (lane == 0) sh.w[s] = acc / A.S;
     }
     __syncthreads();
+}
+
+// The 16 contiguous entries [e0, e0 + 16) of a row, clamped; entries >= Vend are NEG_CLAMP.
+// e0 is a multiple of 16 entries, so whole vectors are 16-byte aligned (rows are, by the ABI).
+template <typename Tin>
+__device__ __forceinline__ void load16(const Tin* row, int64_t e0, int64_t Vend, float* x) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    if (e0 + ET <= Vend) {
+        uint4 v[ET / VEC];
+#pragma unroll
+        for (int jv = 0; jv < ET / VEC; ++jv) v[jv] = __ldg(reinterpret_cast<const uint4*>(row + e0) + jv);
+#pragma unroll
+        for (int jv = 0; jv < ET / VEC; ++jv) unpack_clamped<Tin>(v[jv], &x[jv * VEC]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < ET; ++k) x[k] = (e0 + k < Vend) ? clamp1(Elem<Tin>::load1(row + e0 + k)) : NEG_CLAMP;
+    }
 }
 
 // Weight of vocabulary entry z (and z' for the residual) in float64.
 __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, double B) {
     if (!(za > NEG_MASKED)) return 0.0;
-    const double pa = exp((double)za - A);
+    const double pa = dexp_neg((double)za - A);     // z <= max <= lse: argument <= 0
     if (!resid) return pa;
-    const double qb = (zb > NEG_MASKED) ? exp((double)zb - B) : 0.0;
+    const double qb = (zb > NEG_MASKED) ? dexp_neg((double)zb - B) : 0.0;
     const double r = pa - qb;
     return r > 0.0 ? r : 0.0;
 }
@@ -221,28 +368,15 @@ __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, d
 // Inverse-CDF search inside slice s with weights wt(), given the float64 mass of
 // all earlier slices (`before`) and the target u*Z.  Thread t scans the 16
 // contiguous entries [t*16, t*16+16) of the slice.  Returns the token or -1.
-template <typename Tin>
-__device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A, double B,
-                              int64_t V, int s, int vse, double before, double target, double Z, double u,
-                              TailShared& sh, bool* tie) {
-    const int64_t e0 = (int64_t)s * vse + threadIdx.x * ET;
-    V = min(V, (int64_t)(s + 1) * vse);
-    if (threadIdx.x == 0) sh.near = 0;
-    double w[ET];
+// Block-wide inverse-CDF step over the threads' 16 weights each (fixed order): the first entry
+// whose float64 prefix exceeds `target`; the crossing thread gets its prefix bounds.
+template <typename WF>
+__device__ __forceinline__ int scan_find(WF w, int64_t e0, double before, double target, TailShared& sh,
+                                         int* found, double* cprev_f, double* c_f) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double loc = 0.0;
 #pragma unroll
-    for (int k = 0; k < ET; ++k) {
-        const int64_t v = e0 + k;
-        float za = NEG_CLAMP, zb = NEG_CLAMP;
-        if (v < V) {
-            za = clamp1(Elem<Tin>::load1(ra + v));
-            if (resid) zb = clamp1(Elem<Tin>::load1(rb + v));
-        }
-        w[k] = wt(resid, za, zb, A, B);
-        loc += w[k];
-    }
-    // exclusive scan of per-thread totals (fixed order: serial over warps)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int k = 0; k < ET; ++k) loc += (double)w(k);
     double incl = loc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -255,19 +389,70 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
     double woff = 0.0;
     for (int wi = 0; wi < warp; ++wi) woff += sh.red_d[wi];
     double c = before + woff + (incl - loc);
-    int found = 0x7fffffff;
-    double cprev_f = 0.0, c_f = 0.0;
+    *found = 0x7fffffff;
 #pragma unroll
     for (int k = 0; k < ET; ++k) {
         const double cp = c;
-        c += w[k];
-        if (found == 0x7fffffff && w[k] > 0.0 && c > target) {
-            found = (int)(e0 + k);
-            cprev_f = cp;
-            c_f = c;
+        const double wk = (double)w(k);
+        c += wk;
+        if (*found == 0x7fffffff && wk > 0.0 && c > target) {
+            *found = (int)(e0 + k);
+            *cprev_f = cp;
+            *c_f = c;
         }
     }
-    const int best = block_min_i(found, sh);
+    return block_min_i(*found, sh);
+}
+
+// Inverse-CDF search inside slice s with weights wt(), given the float64 mass of all earlier
+// slices (`before`) and the target u*Z.  Thread t scans the 16 contiguous entries
+// [t*16, t*16+16) of the slice.  Returns the token or -1.
+// Fast pass: fp32 weights (MUFU), float64 prefix; their total error is far below
+// DRAW_MARGIN * Z (Z >= z_safe for residual draws, ~1 for bonus draws), so the crossing token
+// is the exact one unless the target lies within that margin of a boundary -- then the exact
+// pass (float64 weights, the oracle's arithmetic, R5) decides.
+template <typename Tin>
+__device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A, double B,
+                              int64_t V, int s, int vse, double before, double target, double Z, double u,
+                              TailShared& sh, bool* tie) {
+    const int64_t e0 = (int64_t)s * vse + threadIdx.x * ET;
+    V = min(V, (int64_t)(s + 1) * vse);
+    if (threadIdx.x == 0) { sh.near = 0; sh.found = 0; }
+    float xa[ET], xb[ET];
+    load16<Tin>(ra, e0, V, xa);
+    if (resid) load16<Tin>(rb, e0, V, xb);
+    int found;
+    double cprev_f = 0.0, c_f = 0.0;
+    {
+        const float Ah = (float)A, Al = (float)(A - (double)Ah);
+        const float Bh = (float)B, Bl = (float)(B - (double)Bh);
+        float wf[ET];
+#pragma unroll
+        for (int k = 0; k < ET; ++k) {
+            float wk = 0.f;
+            if (xa[k] > NEG_MASKED) {
+                wk = ex2f(((xa[k] - Ah) - Al) * LOG2E);
+                if (resid) {
+                    const float qk = xb[k] > NEG_MASKED ? ex2f(((xb[k] - Bh) - Bl) * LOG2E) : 0.f;
+                    wk = fmaxf(wk - qk, 0.f);
+                }
+            }
+            wf[k] = wk;
+        }
+        const int best = scan_find([&](int k) { return wf[k]; }, e0, before, target, sh, &found, &cprev_f, &c_f);
+        if (best != 0x7fffffff && found == best)
+            sh.found = (fabs(target - cprev_f) < DRAW_MARGIN * Z || fabs(c_f - target) < DRAW_MARGIN * Z) ? 1 : 0;
+        __syncthreads();
+        const bool clear = best != 0x7fffffff && sh.found == 0;
+        __syncthreads();
+        if (clear) {
+            *tie = false;
+            return best;
+        }
+    }
+    // (weights recomputed on demand: this path is rare and registers are not)
+    const int best = scan_find([&](int k) { return wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, A, B); }, e0, before,
+                               target, sh, &found, &cprev_f, &c_f);
     if (best != 0x7fffffff && found == best) {
         *tie = fabs(u - cprev_f / Z) < TIE_EPS || fabs(u - c_f / Z) < TIE_EPS;
         sh.near = *tie ? 1 : 0;
@@ -295,20 +480,36 @@ __device__ int32_t last_positive(bool resid, const Tin* ra, const Tin* rb, doubl
 template <typename Tin>
 __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double A, double B,
                                int64_t V, int C, int vse, double Z, double u, TailShared& sh, bool* tie) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        // first slice whose inclusive float64 prefix exceeds u Z (warp scan, 32 slices a step)
+        const int lane = threadIdx.x;
         const double target = u * Z;
-        double c = 0.0;
-        int sel = -1;
-        int lastpos = -1;
+        double base = 0.0;
+        int sel = -1, lastpos = -1;
         double before = 0.0;
-        for (int s = 0; s < C; ++s) {
-            if (sh.w[s] > 0.0) lastpos = s;
-            if (sel < 0 && sh.w[s] > 0.0 && c + sh.w[s] > target) { sel = s; before = c; }
-            c += sh.w[s];
+        for (int s0 = 0; s0 < C; s0 += 32) {
+            const double ws = (s0 + lane < C) ? sh.w[s0 + lane] : 0.0;
+            double incl = ws;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, ws > 0.0 && base + incl > target);
+            const unsigned pos = __ballot_sync(0xffffffffu, ws > 0.0);
+            if (pos) lastpos = s0 + 31 - __clz((int)pos);
+            if (sel < 0 && hit) {
+                const int f = __ffs((int)hit) - 1;
+                sel = s0 + f;
+                before = base + __shfl_sync(0xffffffffu, incl - ws, f);
+            }
+            base += __shfl_sync(0xffffffffu, incl, 31);
         }
-        if (sel < 0) { sel = -1 - (lastpos < 0 ? 0 : lastpos); before = c; }
-        sh.sel_slice = sel;
-        sh.sel_before = before;
+        if (sel < 0) { sel = -1 - (lastpos < 0 ? 0 : lastpos); before = base; }
+        if (lane == 0) {
+            sh.sel_slice = sel;
+            sh.sel_before = before;
+        }
     }
     __syncthreads();
     const int sel = sh.sel_slice;
@@ -332,10 +533,10 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
     double sa = 0.0, sb = 0.0;
     for (int64_t v = threadIdx.x; v < V; v += T) {
         const float za = clamp1(Elem<Tin>::load1(ra + v));
-        if (za > NEG_MASKED) sa += exp((double)za - Ar.M);
+        if (za > NEG_MASKED) sa += dexp_neg((double)za - Ar.M);
         if (resid) {
             const float zb = clamp1(Elem<Tin>::load1(rb + v));
-            if (zb > NEG_MASKED) sb += exp((double)zb - Br.M);
+            if (zb > NEG_MASKED) sb += dexp_neg((double)zb - Br.M);
         }
     }
     sa = block_sum_d(sa, sh);
@@ -367,13 +568,20 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
 }
 
 template <typename Tin>
-__global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
+#ifndef MSD_TAIL_MINB
+#define MSD_TAIL_MINB 2
+#endif
+__global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
     __shared__ TailShared sh;
     const int64_t b = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int L = p.L, K = p.K, C = p.C;
     const int64_t V = p.V;
 
+    TPROF_DECL
+#ifdef MSD_PROF
+    if (tid == 0 && b < 4096) g_tail_cta[b][0] = globaltimer();
+#endif
     if (tid == 0) {
         sh.flags = 0;
         int m1 = p.m0 ? p.m0[b] : K;
@@ -381,12 +589,35 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         sh.m[1] = m1;
     }
     for (int q = tid; q < MAXL * MAXL; q += T) (&sh.extra_ok[0][0])[q] = 0;
+    // one round trip for everything the request needs from the core and the draft: its slice
+    // partials and residuals into shared memory (when they fit), the draft tokens' logits
+    extern __shared__ __align__(16) unsigned char tdyn[];
+    const size_t npart = (size_t)K * L * C, nres = (size_t)K * (L - 1) * C;
+    const bool pre = p.prefetch != 0;
+    const Partial* part_b = p.partials + (size_t)b * npart;
+    const double* res_b = p.resid + (size_t)b * nres;
+    if (pre) {
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(part_b);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(tdyn);
+        const size_t nw = npart * sizeof(Partial) / 8;
+        for (size_t t = tid; t < nw; t += T) dst[t] = src[t];
+        double* rd = reinterpret_cast<double*>(tdyn + npart * sizeof(Partial));
+        for (size_t t = tid; t < nres; t += T) rd[t] = res_b[t];
+        part_b = reinterpret_cast<const Partial*>(tdyn);
+        res_b = rd;
+    }
+    for (int t = tid; t < L * K; t += T) {
+        const int l = t / K, i = t % K;
+        const int32_t x = p.cand0[b * K + i];
+        sh.zpre[l][i] = (x >= 0 && x < V) ? clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l, b, i) + x)) : NEG_CLAMP;
+    }
+    __syncthreads();
     // row normalisers (Eq. 1) and KL numerators of every draft-position row, combined from
     // the core's slice partials in a fixed order (one warp per row)
     for (int r = warp; r < K * L; r += NWARP) {
         const int i = r / L, l = r % L;
         double Kl;
-        const Partial* pp = p.partials + (((size_t)b * K + i) * L + l) * C;
+        const Partial* pp = part_b + ((size_t)i * L + l) * C;
         RowStat rs = combine_row(pp, C, &Kl, l > 0 ? pp - C : nullptr);
         if (lane == 0) { sh.row[i][l] = rs; sh.kl[i][l] = Kl; }
     }
@@ -405,19 +636,21 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
 
     int64_t st_near[MAXL] = {0, 0, 0, 0}, st_exact[MAXL] = {0, 0, 0, 0};
 
+    TPROF(0)
     for (int l = 1; l < L; ++l) {
         const int m = sh.m[l];
         // rows at positions >= K needed by this level's tests (level l and l-1)
         for (int i = K; i < m; ++i) {
             for (int lv = l - 1; lv <= l; ++lv) {
                 if (!sh.extra_ok[lv][i - K]) {
-                    RowStat r = row_stats<Tin>(row_ptr<Tin>(p, lv, b, i), V, C, p.VSe, sh);
+                    RowStat r = row_stats<Tin>(row_ptr<Tin>(p, lv, b, i), V, C, p.VSe, sh, p.greedy != 0);
                     if (tid == 0) { sh.extra[lv][i - K] = r; sh.extra_ok[lv][i - K] = 1; }
                     __syncthreads();
                 }
             }
         }
         __syncthreads();
+        TPROF(1)
 
         // ---- acceptance tests (warp 0, lane i = position i), first rejection
         if (warp == 0) {
@@ -434,8 +667,9 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
                 } else if (p.greedy) {
                     acc = (t == A.amax);
                 } else {
-                    const float za = clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l, b, i) + t));
-                    const float zb = clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l - 1, b, i) + t));
+                    const bool draft = i < K && t == p.cand0[b * K + i];
+                    const float za = draft ? sh.zpre[l][i] : clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l, b, i) + t));
+                    const float zb = draft ? sh.zpre[l - 1][i] : clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l - 1, b, i) + t));
                     const double u = (double)p.u_acc[(l - 1) * p.ua_l + b * p.ua_b + i];
                     if (!(za > NEG_MASKED)) {
                         acc = false;
@@ -461,12 +695,14 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         __syncthreads();
         const int n = sh.n[l];
 
+        TPROF(2)
         // ---- per-position divergence of pair (l-1, l), i < K
-        for (int i = tid; i < K; i += T) {
-            const size_t u = (size_t)b * K + i;
+        for (int i = warp; i < K; i += NWARP) {   // one warp per position: lanes over slices
             double d = 0.0;
-            const double* R = p.resid + (u * (L - 1) + (l - 1)) * C;
-            for (int s = 0; s < C; ++s) d += R[s];
+            const double* R = res_b + ((size_t)i * (L - 1) + (l - 1)) * C;
+            for (int s = lane; s < C; s += 32) d += R[s];
+            d = warp_sum_d(d);
+            if (lane != 0) continue;
             double kl = sh.kl[i][l];
             const bool kinf = !(kl < KL_INF_THRESH);
             if (kinf) kl = INFINITY;
@@ -485,6 +721,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
             if (kinf) atomicOr(&sh.flags, (uint32_t)MSD_F_KL_INF);
         }
 
+        TPROF(3)
         // ---- emission
         const bool is_final = (l == L - 1);
         const bool resid = n < m;
@@ -500,7 +737,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
                 Bq = sh.row[pos][l - 1];
             } else {
                 if (!resid) {  // bonus row: (re)compute so sh.part holds its slice partials
-                    RowStat r = row_stats<Tin>(ra, V, C, p.VSe, sh);
+                    RowStat r = row_stats<Tin>(ra, V, C, p.VSe, sh, p.greedy != 0);
                     if (tid == 0) { sh.extra[l][pos - K] = r; sh.extra_ok[l][pos - K] = 1; }
                     __syncthreads();
                 }
@@ -516,25 +753,28 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
                 // per-slice weights
                 if (resid) {
                     if (pos < K) {
-                        const double* R = p.resid + (((size_t)b * K + pos) * (L - 1) + (l - 1)) * C;
+                        const double* R = res_b + ((size_t)pos * (L - 1) + (l - 1)) * C;
                         for (int s = tid; s < C; s += T) sh.w[s] = R[s];
                         __syncthreads();
                     } else {
                         pair_resid<Tin>(ra, rb, A, Bq, V, C, p.VSe, sh);
                     }
                 } else {
-                    const Partial* P = p.partials + (((size_t)b * K + pos) * L + l) * C;
+                    const Partial* P = part_b + ((size_t)pos * L + l) * C;
                     for (int s = tid; s < C; s += T) {
                         const Partial pr = pos < K ? P[s] : sh.part[s];
-                        sh.w[s] = pr.S * exp((double)pr.m - A.M) / A.S;
+                        sh.w[s] = pr.S * dexp_neg((double)pr.m - A.M) / A.S;
                     }
                     __syncthreads();
                 }
                 double Z = 0.0;
-                for (int s = 0; s < C; ++s) Z += sh.w[s];
+                for (int s = lane; s < C; s += 32) Z += sh.w[s];
+                Z = warp_sum_d(Z);
+                TPROF(7)
                 y = -1;
                 if (!p.exact_all && (!resid || Z >= p.z_safe))
                     y = draw_slices<Tin>(resid, ra, rb, A.lse, Bq.lse, V, C, p.VSe, Z, u, sh, &tie);
+                TPROF(8)
                 if (y < 0) {
                     exact = true;
                     tie = false;
@@ -549,6 +789,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
             }
             __syncthreads();
         }
+        TPROF(4)
         // ---- next candidate list
         if (tid == 0) {
             for (int i = 0; i < n; ++i) sh.c[l + 1][i] = sh.c[l][i];
@@ -558,6 +799,7 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
         __syncthreads();
     }
 
+    TPROF(5)
     // ---- outputs, rollback lengths, stats, counter reset
     const int clen = sh.m[L];
     for (int j = tid; j < p.out_ld; j += T) p.out_tok[b * p.out_ld + j] = j < clen ? sh.c[L][j] : -1;
@@ -592,15 +834,40 @@ __global__ void __launch_bounds__(T) tail_kernel(TailParams p) {
     for (int i = tid; i < K; i += T) p.cnt[((size_t)b * K + i) * CNT_STRIDE] = 0u;
     unsigned long long* pm = reinterpret_cast<unsigned long long*>(p.partms) + (size_t)b * K * L * C;
     for (int t = tid; t < K * L * C; t += T) pm[t] = 0ull;
+    TPROF(6)
+#ifdef MSD_PROF
+    if (tid == 0 && b < 4096) g_tail_cta[b][1] = globaltimer();
+#endif
 }
 
-cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s) {
-    if (p.B <= 0) return cudaSuccess;
-    if (bf16)
-        tail_kernel<__nv_bfloat16><<<p.B, T, 0, s>>>(p);
-    else
-        tail_kernel<float><<<p.B, T, 0, s>>>(p);
+cudaError_t launch_tail(const TailParams& p0, int bf16, cudaStream_t s) {
+    if (p0.B <= 0) return cudaSuccess;
+    TailParams p = p0;
+    const size_t dyn = (size_t)p.K * p.L * p.C * sizeof(Partial) + (size_t)p.K * (p.L - 1) * p.C * sizeof(double);
+    p.prefetch = dyn <= TAIL_DYN_MAX ? 1 : 0;
+    const size_t smem = p.prefetch ? dyn : 0;
+    auto k = bf16 ? tail_kernel<__nv_bfloat16> : tail_kernel<float>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TAIL_DYN_MAX);
+    if (e != cudaSuccess) return e;
+    k<<<p.B, T, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 }  // namespace msd
+
+#ifdef MSD_PROF
+extern "C" int msd_debug_tail_req(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, msd::g_tail_req, sizeof(unsigned long long) * 4096 * 16) != cudaSuccess;
+}
+extern "C" int msd_debug_tail_cta(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, msd::g_tail_cta, sizeof(unsigned long long) * 4096 * 2) != cudaSuccess;
+}
+extern "C" int msd_debug_tail_prof(unsigned long long* out16, int reset) {
+    if (cudaMemcpyFromSymbol(out16, msd::g_tail_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[16] = {};
+        if (cudaMemcpyToSymbol(msd::g_tail_prof, z, sizeof(z)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+#endif
