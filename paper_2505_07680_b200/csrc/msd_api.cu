@@ -168,7 +168,7 @@ msd_status run_engine(const Engine& E) {
     tp.pos_dtv = E.pos_dtv; tp.pos_kl = E.pos_kl; tp.stats = E.stats; tp.flags = E.flags;
     tp.partials = cp.partials; tp.partms = cp.partms; tp.resid = cp.resid;
     tp.cnt = cp.cnt;
-    tp.z_safe = env_double("MSD_Z_SAFE", 0.05);
+    tp.z_safe = env_double("MSD_Z_SAFE", 0.05);   // exact draws below this residual mass (R4)
     tp.exact_all = (int32_t)env_double("MSD_EXACT_DRAWS", 0.0);
 
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};

@@ -1035,7 +1035,9 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     // item pattern: T items use the NT TMEM slots; R items keep their ring stage.  Of the S
     // stages ~4 are needed in flight for the TMA; the rest may hold R items.
     int pt = env_int("MSD_PAT_T", NT), pr = env_int("MSD_PAT_R", -1);
-    if (pr < 0) pr = std::max(0, std::min(NT, S - 5));
+    // measured on B200 (tools/core_sweep.py, Llama-3): 2 kept-ring items per 5 TMEM items is
+    // best; more R items cost MUFU recomputation, fewer leave the exchange latency exposed
+    if (pr < 0) pr = std::max(0, std::min(2, S - 5));
     if (pt < 1) pt = 1;
     p.pat_t = pt;
     p.pat_p = pt + pr;

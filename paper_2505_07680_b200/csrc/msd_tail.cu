@@ -10,7 +10,8 @@
 // mass R_s of each 4096-entry vocabulary slice (and the slice partials from which
 // the bonus mass P_s follows).  A draw picks the slice from these (float64
 // prefix) and rescans only that slice in float64 (`draw_fast`).  When the
-// residual mass is small (Z < z_safe) the fp32-derived slice masses are not
+// residual mass is small (Z < z_safe, default 0.05) or the target is within the margin of a
+// slice / token boundary, the fp32-derived slice masses are not
 // accurate enough relative to Z, so the whole row pair is recomputed in float64
 // (`draw_exact`, flagged MSD_F_EXACT_DRAW).  Rows at positions >= K (bonus rows,
 // needed only when a level accepts everything) are computed on demand here.
@@ -32,7 +33,10 @@ __device__ unsigned long long g_tail_req[4096][16];  // per request: cycles per 
 #define TPROF(k)
 #endif
 constexpr double TIE_EPS = 1e-6;
-constexpr double DRAW_MARGIN = 2e-5;   // fp32 draw weights: decide only crossings this far (x Z) from a boundary
+// Fast-path draws (Z >= z_safe) decide a crossing only when it is farther than DRAW_MARGIN * Z
+// from the chosen slice's and token's boundaries; the fp32-derived masses drift by ~3e-8 / Z
+// (R4), far inside the margin.  Otherwise the exact path decides.
+constexpr double DRAW_MARGIN_REL = 2e-5, DRAW_MARGIN_ABS = 0.0;
 
 struct TailShared {
     RowStat row[MAXC][MAXL];      // row statistics of draft positions i < K (from the core partials)
@@ -408,13 +412,13 @@ __device__ __forceinline__ int scan_find(WF w, int64_t e0, double before, double
 // slices (`before`) and the target u*Z.  Thread t scans the 16 contiguous entries
 // [t*16, t*16+16) of the slice.  Returns the token or -1.
 // Fast pass: fp32 weights (MUFU), float64 prefix; their total error is far below
-// DRAW_MARGIN * Z (Z >= z_safe for residual draws, ~1 for bonus draws), so the crossing token
+// the draw margins (DRAW_MARGIN_REL * Z + DRAW_MARGIN_ABS), so the crossing token
 // is the exact one unless the target lies within that margin of a boundary -- then the exact
 // pass (float64 weights, the oracle's arithmetic, R5) decides.
 template <typename Tin>
 __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A, double B,
                               int64_t V, int s, int vse, double before, double target, double Z, double u,
-                              TailShared& sh, bool* tie) {
+                              TailShared& sh, bool* tie, bool exact_only = false) {
     const int64_t e0 = (int64_t)s * vse + threadIdx.x * ET;
     V = min(V, (int64_t)(s + 1) * vse);
     if (threadIdx.x == 0) { sh.near = 0; sh.found = 0; }
@@ -423,7 +427,7 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
     if (resid) load16<Tin>(rb, e0, V, xb);
     int found;
     double cprev_f = 0.0, c_f = 0.0;
-    {
+    if (!exact_only) {
         const float Ah = (float)A, Al = (float)(A - (double)Ah);
         const float Bh = (float)B, Bl = (float)(B - (double)Bh);
         float wf[ET];
@@ -441,7 +445,8 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
         }
         const int best = scan_find([&](int k) { return wf[k]; }, e0, before, target, sh, &found, &cprev_f, &c_f);
         if (best != 0x7fffffff && found == best)
-            sh.found = (fabs(target - cprev_f) < DRAW_MARGIN * Z || fabs(c_f - target) < DRAW_MARGIN * Z) ? 1 : 0;
+            sh.found = (fabs(target - cprev_f) < DRAW_MARGIN_REL * Z + DRAW_MARGIN_ABS ||
+                        fabs(c_f - target) < DRAW_MARGIN_REL * Z + DRAW_MARGIN_ABS) ? 1 : 0;
         __syncthreads();
         const bool clear = best != 0x7fffffff && sh.found == 0;
         __syncthreads();
@@ -449,6 +454,7 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
             *tie = false;
             return best;
         }
+        // within the margin of a token boundary: the float64 rescan below decides
     }
     // (weights recomputed on demand: this path is rare and registers are not)
     const int best = scan_find([&](int k) { return wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, A, B); }, e0, before,
@@ -479,7 +485,8 @@ __device__ int32_t last_positive(bool resid, const Tin* ra, const Tin* rb, doubl
 // prefix, rescan it.  Returns token or -1 (inconsistent -> caller goes exact).
 template <typename Tin>
 __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double A, double B,
-                               int64_t V, int C, int vse, double Z, double u, TailShared& sh, bool* tie) {
+                               int64_t V, int C, int vse, double Z, double u, TailShared& sh, bool* tie,
+                               bool exact = false) {
     if (threadIdx.x < 32) {
         // first slice whose inclusive float64 prefix exceeds u Z (warp scan, 32 slices a step)
         const int lane = threadIdx.x;
@@ -519,49 +526,67 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
         *tie = true;
         return last_positive<Tin>(resid, ra, rb, A, B, V, -1 - sel, vse, sh);
     }
-    return scan_slice<Tin>(resid, ra, rb, A, B, V, sel, vse, before, u * Z, Z, u, sh, tie);
+    return scan_slice<Tin>(resid, ra, rb, A, B, V, sel, vse, before, u * Z, Z, u, sh, tie, exact);
 }
 
-// Exact float64 draw over the whole row (pair): exact normalisers, exact slice
-// masses, exact scan.  Residual mass < 1e-12 -> draw from p.
+// Exact float64 draw over the whole row (pair): exact normalisers, exact slice masses (one
+// warp per slice, fixed order), exact scan.  Residual mass < 1e-12 -> draw from p.
 template <typename Tin>
 __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const RowStat& Ar,
                               const RowStat& Br, int64_t V, int C, int vse, double u, TailShared& sh,
                               bool* tie, bool* small) {
+  constexpr int VEC = Elem<Tin>::VEC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // exact normalisers: every thread a strided set of whole vectors, 4 in flight
+  double sa = 0.0, sb = 0.0;
+  {
+      constexpr int U = 4;
+      for (int64_t e0 = (int64_t)threadIdx.x * VEC; e0 < V; e0 += (int64_t)U * T * VEC) {
+          float xa[U][VEC], xb[U][VEC];
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu) {
+              load_vec<Tin>(ra, e0 + (int64_t)uu * T * VEC, V, xa[uu]);
+              if (resid) load_vec<Tin>(rb, e0 + (int64_t)uu * T * VEC, V, xb[uu]);
+          }
+#pragma unroll
+          for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+              for (int k = 0; k < VEC; ++k) {
+                  if (xa[uu][k] > NEG_MASKED) sa += dexp_neg((double)xa[uu][k] - Ar.M);
+                  if (resid && xb[uu][k] > NEG_MASKED) sb += dexp_neg((double)xb[uu][k] - Br.M);
+              }
+          }
+      }
+  }
+  sa = block_sum_d(sa, sh);
+  if (resid) sb = block_sum_d(sb, sh);
+  const double A = Ar.M + log(sa);
+  const double B0 = resid ? Br.M + log(sb) : 0.0;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    // exact normalisers
-    double sa = 0.0, sb = 0.0;
-    for (int64_t v = threadIdx.x; v < V; v += T) {
-        const float za = clamp1(Elem<Tin>::load1(ra + v));
-        if (za > NEG_MASKED) sa += dexp_neg((double)za - Ar.M);
-        if (resid) {
-            const float zb = clamp1(Elem<Tin>::load1(rb + v));
-            if (zb > NEG_MASKED) sb += dexp_neg((double)zb - Br.M);
-        }
-    }
-    sa = block_sum_d(sa, sh);
-    if (resid) sb = block_sum_d(sb, sh);
-    const double A = Ar.M + log(sa);
-    const double B = resid ? Br.M + log(sb) : 0.0;
-    for (int s = 0; s < C; ++s) {
+    const double B = resid ? B0 : 0.0;
+    for (int s = warp; s < C; s += NWARP) {
+        const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
         double acc = 0.0;
-        for (int64_t v = (int64_t)s * vse + threadIdx.x; v < min(V, (int64_t)(s + 1) * vse); v += T) {
-            const float za = clamp1(Elem<Tin>::load1(ra + v));
-            const float zb = resid ? clamp1(Elem<Tin>::load1(rb + v)) : NEG_CLAMP;
-            acc += wt(resid, za, zb, A, B);
+        for (int64_t e = s0 + (int64_t)lane * VEC; e < s1; e += 32 * VEC) {
+            float xa[VEC], xb[VEC];
+            load_vec<Tin>(ra, e, s1, xa);
+            if (resid) load_vec<Tin>(rb, e, s1, xb);
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, A, B);
         }
-        acc = block_sum_d(acc, sh);
-        if (threadIdx.x == 0) sh.w[s] = acc;
+        acc = warp_sum_d(acc);
+        if (lane == 0) sh.w[s] = acc;
     }
     __syncthreads();
     double Z = 0.0;
-    for (int s = 0; s < C; ++s) Z += sh.w[s];
+    for (int s = lane; s < C; s += 32) Z += sh.w[s];
+    Z = warp_sum_d(Z);
     if (resid && Z < 1e-12) {   // residual vanished -> draw from p
         *small = true;
         resid = false;
         continue;
     }
-    int32_t y = draw_slices<Tin>(resid, ra, rb, A, B, V, C, vse, Z, u, sh, tie);
+    int32_t y = draw_slices<Tin>(resid, ra, rb, A, B, V, C, vse, Z, u, sh, tie, /*exact=*/true);
     return y < 0 ? 0 : y;
   }
   return 0;

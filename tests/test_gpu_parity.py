@@ -48,6 +48,17 @@ def test_configs_match_oracle(name, kw):
     print(name, rep)
 
 
+@pytest.mark.parametrize("pat_t,pat_r", [(5, 0), (1, 6), (3, 2)])
+def test_item_patterns_agree(monkeypatch, pat_t, pat_r):
+    """T items (exponentials parked in TMEM) and R items (ring stage kept, pass 2 recomputes)
+    must give the same accept / emit decisions and divergences as the oracle, in any mix."""
+    inp = _gauss("llama3", B=24, V=30000)
+    monkeypatch.setenv("MSD_PAT_T", str(pat_t))
+    monkeypatch.setenv("MSD_PAT_R", str(pat_r))
+    o = _run(inp)
+    assert_parity(o, run_oracle(inp))
+
+
 @pytest.mark.parametrize("name,kw", [("tiny", {}), ("llama3", dict(B=12, V=40000)),
                                       ("sweep", dict(B=6, V=9000))])
 def test_greedy_matches_oracle(name, kw):
