@@ -170,6 +170,10 @@ msd_status run_engine(const Engine& E) {
     tp.cnt = cp.cnt;
     tp.z_safe = env_double("MSD_Z_SAFE", 0.05);   // exact draws below this residual mass (R4)
     tp.exact_all = (int32_t)env_double("MSD_EXACT_DRAWS", 0.0);
+    {
+        cudaError_t te = exp_table(&tp.exptab);
+        if (te != cudaSuccess) return cuda_fail(te, "exp table");
+    }
 
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     {

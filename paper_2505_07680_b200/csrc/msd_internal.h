@@ -44,6 +44,8 @@ struct CoreParams {
 
 // the constant pad buffer of the current device (filled on first use)
 cudaError_t core_pad(const void** out);
+// exp of every bf16 value in float64 (65536 entries, filled on first use per device)
+cudaError_t exp_table(const double** out);
 
 struct TailParams {
     LevelDesc lv;
@@ -72,6 +74,7 @@ struct TailParams {
     double z_safe;
     int32_t exact_all;
     int32_t prefetch;   // set by launch_tail: partials + residuals of a request fit in shared memory
+    const double* exptab;   // exp of every bf16 value (exact-draw path), from exp_table()
 };
 
 struct RollbackParams {

@@ -59,6 +59,7 @@ struct TailShared {
     double sel_before;
     int32_t sel_slice;
     float zpre[MAXL][MAXC];       // z_l[b, i, x_i]: the draft token's logit in every row i < K
+    const double* exptab;         // exp of every bf16 value (float64), or NULL
 };
 constexpr size_t TAIL_DYN_MAX = 96 * 1024;   // prefetched partials + slice residuals
 
@@ -360,11 +361,39 @@ __device__ __forceinline__ void load16(const Tin* row, int64_t e0, int64_t Vend,
 }
 
 // Weight of vocabulary entry z (and z' for the residual) in float64.
+// exp(z - S) in float64.  For bf16 logits (every z is a bf16 value) it is tab[bits(z)] * e^-S
+// with tab[h] = exp(bf16 h) (msd_api: exp_table), one lookup and one multiply instead of a
+// float64 exp; outside the table's range (|z| >= 700, |S| >= 700) the FMA-pipe dexp_neg.
+struct ExpShift {
+    const double* tab;   // NULL: no table (f32 logits)
+    double S, eS;
+    __device__ void init(const double* t, double s_) {
+        tab = (t && fabs(s_) < 700.0) ? t : nullptr;
+        S = s_;
+        eS = tab ? exp(-s_) : 0.0;
+    }
+    __device__ __forceinline__ double operator()(float z) const {
+        if (tab) {
+            const double t = __ldg(tab + (__float_as_uint(z) >> 16));
+            if (t == t) return t * eS;      // NaN entry: outside the table's range
+        }
+        return dexp_neg((double)z - S);     // z <= max <= S: argument <= 0
+    }
+};
+
 __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, double B) {
     if (!(za > NEG_MASKED)) return 0.0;
     const double pa = dexp_neg((double)za - A);     // z <= max <= lse: argument <= 0
     if (!resid) return pa;
     const double qb = (zb > NEG_MASKED) ? dexp_neg((double)zb - B) : 0.0;
+    const double r = pa - qb;
+    return r > 0.0 ? r : 0.0;
+}
+__device__ __forceinline__ double wt(bool resid, float za, float zb, const ExpShift& ea, const ExpShift& eb) {
+    if (!(za > NEG_MASKED)) return 0.0;
+    const double pa = ea(za);
+    if (!resid) return pa;
+    const double qb = (zb > NEG_MASKED) ? eb(zb) : 0.0;
     const double r = pa - qb;
     return r > 0.0 ? r : 0.0;
 }
@@ -457,8 +486,11 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
         // within the margin of a token boundary: the float64 rescan below decides
     }
     // (weights recomputed on demand: this path is rare and registers are not)
-    const int best = scan_find([&](int k) { return wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, A, B); }, e0, before,
-                               target, sh, &found, &cprev_f, &c_f);
+    ExpShift ea, eb;
+    ea.init(sizeof(Tin) == 2 ? sh.exptab : nullptr, A);
+    eb.init(sizeof(Tin) == 2 ? sh.exptab : nullptr, B);
+    const int best = scan_find([&](int k) { return wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, ea, eb); }, e0,
+                               before, target, sh, &found, &cprev_f, &c_f);
     if (best != 0x7fffffff && found == best) {
         *tie = fabs(u - cprev_f / Z) < TIE_EPS || fabs(u - c_f / Z) < TIE_EPS;
         sh.near = *tie ? 1 : 0;
@@ -537,7 +569,14 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
                               bool* tie, bool* small) {
   constexpr int VEC = Elem<Tin>::VEC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef MSD_PROF
+  if (threadIdx.x == 0) g_tail_req[blockIdx.x][11] += (unsigned long long)clock64();
+#endif
   // exact normalisers: every thread a strided set of whole vectors, 4 in flight
+  const double* tab = sizeof(Tin) == 2 ? sh.exptab : nullptr;
+  ExpShift eMa, eMb;
+  eMa.init(tab, Ar.M);
+  eMb.init(tab, Br.M);
   double sa = 0.0, sb = 0.0;
   {
       constexpr int U = 4;
@@ -552,32 +591,49 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
           for (int uu = 0; uu < U; ++uu) {
 #pragma unroll
               for (int k = 0; k < VEC; ++k) {
-                  if (xa[uu][k] > NEG_MASKED) sa += dexp_neg((double)xa[uu][k] - Ar.M);
-                  if (resid && xb[uu][k] > NEG_MASKED) sb += dexp_neg((double)xb[uu][k] - Br.M);
+                  if (xa[uu][k] > NEG_MASKED) sa += eMa(xa[uu][k]);
+                  if (resid && xb[uu][k] > NEG_MASKED) sb += eMb(xb[uu][k]);
               }
           }
       }
   }
   sa = block_sum_d(sa, sh);
   if (resid) sb = block_sum_d(sb, sh);
+#ifdef MSD_PROF
+  long long _dx0 = clock64();
+  if (threadIdx.x == 0) g_tail_req[blockIdx.x][9] += (unsigned long long)_dx0;
+#endif
   const double A = Ar.M + log(sa);
   const double B0 = resid ? Br.M + log(sb) : 0.0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     const double B = resid ? B0 : 0.0;
+    ExpShift eA, eB;
+    eA.init(tab, A);
+    eB.init(tab, B);
     for (int s = warp; s < C; s += NWARP) {
         const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
         double acc = 0.0;
-        for (int64_t e = s0 + (int64_t)lane * VEC; e < s1; e += 32 * VEC) {
-            float xa[VEC], xb[VEC];
-            load_vec<Tin>(ra, e, s1, xa);
-            if (resid) load_vec<Tin>(rb, e, s1, xb);
+        constexpr int U = 4;    // vector pairs in flight per lane (HBM round trips dominate)
+        for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
+            float xa[U][VEC], xb[U][VEC];
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, A, B);
+            for (int uu = 0; uu < U; ++uu) {
+                load_vec<Tin>(ra, e0 + (int64_t)uu * 32 * VEC, s1, xa[uu]);
+                if (resid) load_vec<Tin>(rb, e0 + (int64_t)uu * 32 * VEC, s1, xb[uu]);
+            }
+#pragma unroll
+            for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[uu][k], resid ? xb[uu][k] : NEG_CLAMP, eA, eB);
+            }
         }
         acc = warp_sum_d(acc);
         if (lane == 0) sh.w[s] = acc;
     }
     __syncthreads();
+#ifdef MSD_PROF
+    if (threadIdx.x == 0) g_tail_req[blockIdx.x][10] += (unsigned long long)clock64();
+#endif
     double Z = 0.0;
     for (int s = lane; s < C; s += 32) Z += sh.w[s];
     Z = warp_sum_d(Z);
@@ -609,6 +665,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
 #endif
     if (tid == 0) {
         sh.flags = 0;
+        sh.exptab = p.exptab;
         int m1 = p.m0 ? p.m0[b] : K;
         m1 = max(0, min(m1, K));
         sh.m[1] = m1;
@@ -863,6 +920,33 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
 #ifdef MSD_PROF
     if (tid == 0 && b < 4096) g_tail_cta[b][1] = globaltimer();
 #endif
+}
+
+// tab[h] = exp(bf16 with bits h) in float64; NaN where |z| >= 700 or z is not finite
+__global__ void exp_table_kernel(double* tab) {
+    const uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= 65536u) return;
+    const float z = __uint_as_float(h << 16);
+    tab[h] = (isfinite(z) && fabsf(z) < 700.f) ? exp((double)z) : __longlong_as_double(0x7FF8000000000000LL);
+}
+__device__ double g_exptab[65536];
+
+cudaError_t exp_table(const double** out) {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    void* ptr = nullptr;
+    e = cudaGetSymbolAddress(&ptr, g_exptab);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+        exp_table_kernel<<<256, 256>>>(reinterpret_cast<double*>(ptr));
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return e;
+        done[dev] = true;
+    }
+    *out = reinterpret_cast<const double*>(ptr);
+    return cudaSuccess;
 }
 
 cudaError_t launch_tail(const TailParams& p0, int bf16, cudaStream_t s) {

@@ -42,6 +42,9 @@ req1 = (ctypes.c_ulonglong * (4096 * 16))()
 lib.msd_debug_tail_req(req1)
 rq = (np.frombuffer(req1, dtype=np.uint64).astype(np.float64) - np.frombuffer(req0, dtype=np.uint64).astype(np.float64)).reshape(4096, 16)[:B]
 for r in order[:3]:
+    t11, t9, t10 = rq[r, 11], rq[r, 9], rq[r, 10]
+    if t11 > 0:
+        print(f"  req {r} exact draw: normalisers {t9 - t11:.0f} cycles, weights {t10 - t9:.0f}")
     print(f"  req {r} phases (cycles): " + "  ".join(f"{n} {rq[r, k]:.0f}" for k, n in enumerate(names)))
 med = np.argsort(dur)[B // 2]
 print(f"  median req {med} phases (cycles): " + "  ".join(f"{n} {rq[med, k]:.0f}" for k, n in enumerate(names)))
