@@ -66,14 +66,15 @@ def launches(src, out):
         n = r[h.index("Kernel Name")]
         v = float(r[h.index("Metric Value")].replace(",", ""))
         agg.setdefault(n, []).append(v)
-    tot = sum(sum(v) for n, v in agg.items() if "msd::" in n)
+    ours = lambda n: "msd::" in n or any(k in n for k in ("core_kernel", "tail_kernel", "rollback_kernel", "exp_table_kernel"))
+    tot = sum(sum(v) for n, v in agg.items() if ours(n))
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "launches", "avg_ns", "min_ns", "max_ns", "share_of_msd_time"])
         for n, v in agg.items():
-            if "msd::" in n:
+            if ours(n):
                 w.writerow([n, len(v), round(sum(v) / len(v)), round(min(v)), round(max(v)), round(sum(v) / tot, 4)])
-        others = [x for n, v in agg.items() if "msd::" not in n for x in v]
+        others = [x for n, v in agg.items() if not ours(n) for x in v]
         w.writerow(["(torch input generation, outside the timed region)", len(others), "", "", "", ""])
 
 if __name__ == "__main__":
