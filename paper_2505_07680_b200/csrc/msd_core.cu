@@ -695,9 +695,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     if (v == 0 && lane == 0) stamp(j, 12);
                     PROF(1)
                     const Tin* stage = ring + (size_t)cu.st * L * RS;
+                    const bool skip_r = (p.dbg & 2) != 0;   // debug: R items skip the recomputation
 #pragma unroll
                     for (int h = 0; h < NPR; ++h) {
-                        if (h < nreg) {
+                        if (h < nreg && !skip_r) {
                             const int w = v + h * NCW2;
                             const bool clamp = ((cw >> w) & 1u) || ES == 4;
                             float eprev[CET];
