@@ -56,12 +56,15 @@ constexpr int CTH = NCW * 32;          // pass-1 threads
 constexpr int CET = VS / CTH;          // elements per pass-1 thread per row (16)
 constexpr int WCH = CET * 32;          // contiguous slice entries per pass-1 warp (512)
 constexpr int TCOLS = 256;             // TMEM columns per region (2 regions per lane quadrant)
-constexpr int NFETCH = 2;
+#ifndef MSD_NFETCH
+#define MSD_NFETCH 2
+#endif
+constexpr int NFETCH = MSD_NFETCH;
 // Warp numbering: latency-critical service warps first, then pass 2, then the throughput
 // warps (pass 1).  Pass-1 warp W_P1 + r owns region r in TMEM lane quadrant r % 4; pass-2
 // warp W_P2 + v serves regions v and v + 4 (quadrant v): both bases are multiples of 4.
 constexpr int W_PROD = 0, W_PUB = 1, W_FETCH0 = 2, W_RED = W_FETCH0 + NFETCH;
-constexpr int W_P2 = 8, W_P1 = W_P2 + NCW2;
+constexpr int W_P2 = (W_RED + 1 + 3) / 4 * 4, W_P1 = W_P2 + NCW2;   // (4 with one fetcher: 28 warps, 72 registers)
 constexpr int NG1 = 2;                 // pass-1 warp groups: group g processes items j = g mod NG1
 constexpr int CORE_THREADS = (W_P1 + NG1 * NCW) * 32;
 static_assert(W_RED < W_P2 && W_P2 % 4 == 0 && W_P1 % 4 == 0 && NCW % NCW2 == 0 && NCW2 % 4 == 0, "warp roles");
