@@ -67,6 +67,8 @@ def lib() -> ctypes.CDLL:
         L.or_predict_chain_latency.argtypes = [i32, P, P, i32, i32, i32]
         L.or_select_chain.restype = i32
         L.or_select_chain.argtypes = [i32, P, P, i32, i32, i32, i32, P, P]
+        L.or_pool_divergence.restype = None
+        L.or_pool_divergence.argtypes = [P, i32, i32, i32, i64, P, P]
         _ = u32
         _lib = L
     return _lib
@@ -249,3 +251,32 @@ def select_chain(T, sim, W, max_len=4, verify_linear=False, intermediate_bonus=T
     n = lib().or_select_chain(P, _p(T), _p(sim), int(W), int(max_len), int(verify_linear),
                               int(intermediate_bonus), _p(out), ctypes.byref(te))
     return [int(x) for x in out[:n]], te.value
+
+
+def pool_divergence(levels):
+    """SimScore bootstrap divergences: levels = N arrays [B][K][V] (pool models'
+    logits at the same K positions, bf16 values as float) -> (dtv, kl), each
+    [N(N-1)/2][B][K] float64, pairs (i < j) in lexicographic order, KL(p_j || p_i)."""
+    zs = [_f64(z) for z in levels]
+    N = len(zs)
+    B, K, V = zs[0].shape
+    arr = (_Level * N)(*[_Level(z.ctypes.data, z.shape[2], z.shape[1] * z.shape[2], z.shape[1]) for z in zs])
+    npair = N * (N - 1) // 2
+    dtv = np.zeros((npair, B, K)); kl = np.zeros((npair, B, K))
+    lib().or_pool_divergence(ctypes.addressof(arr), N, B, K, V, _p(dtv), _p(kl))
+    return dtv, kl
+
+
+def bootstrap_sim(levels):
+    """Pairwise SimScore matrix [N][N] initialised from the bootstrap (every (i, j)
+    SimScore with observation count 1): sim[i][j] = sim[j][i] = 1 - mean DTV over the
+    positions; 1 on the diagonal."""
+    dtv, _ = pool_divergence(levels)
+    N = len(levels)
+    sim = np.eye(N)
+    pi = 0
+    for i in range(N):
+        for j in range(i + 1, N):
+            sim[i, j] = sim[j, i] = 1.0 - float(dtv[pi].mean())
+            pi += 1
+    return sim

@@ -455,3 +455,30 @@ int32_t or_select_chain(int32_t P, const double* T, const double* sim, int32_t W
     if (t_eff_out) *t_eff_out = best;
     return best_len;
 }
+
+/* SimScore bootstrap ("bootstrap(prefill dists per model) ->
+ * initialized pairwise SimScores"; "initial logits used by the scheduler for baseline
+ * similarity calculations").  For every pair (i < j) of the N pool models, in lexicographic
+ * pair order, and every position k < K of every request b: DTV(p_i, p_j) by Eq. 5 literally
+ * (or_dtv) and KL(p_j || p_i) (the later / larger model against the earlier one, the
+ * verifier || proposer direction of reading R9, or_kl).  Outputs [npairs][B][K]. */
+void or_pool_divergence(const or_level* lv, int32_t N, int32_t B, int32_t K, int64_t V,
+                        double* dtv, double* kl) {
+    const int32_t np = N * (N - 1) / 2;
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t bk = 0; bk < (int64_t)B * K; ++bk) {
+        const int64_t b = bk / K, k = bk % K;
+        double lse[32];
+        for (int32_t l = 0; l < N; ++l) lse[l] = or_lse(lv[l].z + b * lv[l].bstride + k * lv[l].ld, V);
+        int32_t pi = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            for (int32_t j = i + 1; j < N; ++j, ++pi) {
+                const double* zi = lv[i].z + b * lv[i].bstride + k * lv[i].ld;
+                const double* zj = lv[j].z + b * lv[j].bstride + k * lv[j].ld;
+                dtv[((int64_t)pi * B + b) * K + k] = or_dtv(zj, lse[j], zi, lse[i], V);
+                kl[((int64_t)pi * B + b) * K + k] = or_kl(zj, lse[j], zi, lse[i], V);
+            }
+        }
+        (void)np;
+    }
+}

@@ -96,6 +96,13 @@ int32_t or_select_chain(int32_t P, const double* T, const double* sim, int32_t W
                         int32_t verify_linear, int32_t intermediate_bonus,
                         int32_t* chain_out, double* t_eff_out);
 
+/* SimScore bootstrap: per pool pair (i < j, lexicographic) and position,
+ * DTV(p_i, p_j) (Eq. 5) and KL(p_j || p_i); outputs [N(N-1)/2][B][K].  Pinned by
+ * tests/test_oracle_pool.py (identical models, hand-computed pair, mixture closed form,
+ * adjacent pairs equal or_chain_verify's divergences, scipy KL). */
+void or_pool_divergence(const or_level* lv, int32_t N, int32_t B, int32_t K, int64_t V,
+                        double* dtv, double* kl);
+
 #ifdef __cplusplus
 }
 #endif
