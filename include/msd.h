@@ -219,6 +219,25 @@ double msd_simscore_update(double sim, const msd_pair_stats* step_stats, double 
                            int32_t first);
 
 /* ---------------------------------------------------------------------------
+ * msd_pool_divergence -- SimScore bootstrap of an N-model pool (
+ *    S:472-480 "bootstrap(prefill dists per model) -> initialized pairwise SimScores",
+ *    P:152 "initial logits used by the scheduler for baseline similarity calculations").
+ *
+ * models[N] (HOST array, 2 <= N <= 4, capability order): logits [B][rows >= K][ld] of every
+ *    pool model at the same K positions (same dtype, V <= ld, 16-byte aligned rows).
+ * For every position (b, k) and pair (i < j), in lexicographic pair order q:
+ *    pos_dtv[q][b][k] = DTV(p_i, p_j)  (Eq. 5)    (device f32, NULL ok)
+ *    pos_kl[q][b][k]  = KL(p_j || p_i) in nats (reading R9)  (device f32, NULL ok)
+ *    stats[q] += int64 fixed-point sums as in msd_chain_verify (device, NULL ok):
+ *       SimScore_ij = 1 - dtv_fx / (positions * 2^32) initialises every pair.
+ * flags[B] (device, NULL ok): NONFINITE for a row without finite maximum, KL_INF.
+ * Asynchronous on `stream`; no workspace.  Not on the per-step path: reads every row twice.
+ * ------------------------------------------------------------------------- */
+msd_status msd_pool_divergence(const msd_logits* models, int32_t N, int32_t B, int32_t K, int64_t V,
+                               float* pos_dtv, float* pos_kl, msd_pair_stats* stats, uint32_t* flags,
+                               void* stream);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics.
  * msd_last_error: thread-local message for the last non-OK status of this thread.
  * msd_prof_enable(1): record CUDA events around every msd_core launch (the

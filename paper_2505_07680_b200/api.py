@@ -76,6 +76,8 @@ def lib() -> ctypes.CDLL:
     L.msd_verify_level_workspace.argtypes = [i32, i32, i64]
     L.msd_kv_rollback.restype = i32
     L.msd_kv_rollback.argtypes = [P, i32, i32, P, P, P]
+    L.msd_pool_divergence.restype = i32
+    L.msd_pool_divergence.argtypes = [P, i32, i32, i32, i64, P, P, P, P, P]
     L.msd_predict_chain_latency.restype = i32
     L.msd_predict_chain_latency.argtypes = [i32, P, P, i32, i32, i32, P]
     L.msd_select_chain.restype = i32
@@ -246,6 +248,30 @@ class KVRollback:
 
 def kv_rollback(kv: List[dict], rollback: torch.Tensor, flags: torch.Tensor, stream=None):
     KVRollback(kv, rollback, flags)(stream)
+
+
+def pool_divergence(models: Sequence[torch.Tensor], K: Optional[int] = None, V: Optional[int] = None,
+                    stats: bool = True, stream=None) -> dict:
+    """msd_pool_divergence: SimScore bootstrap of an N-model pool.
+    models: N tensors [B][rows >= K][ld] (same dtype); returns device tensors pos_dtv / pos_kl
+    [N(N-1)/2, B, K] (pairs i < j in lexicographic order; KL(p_j || p_i)), stats
+    [N(N-1)/2, 8] int64 and flags [B]."""
+    N = len(models)
+    B = models[0].shape[0]
+    K = models[0].shape[1] if K is None else K
+    V = models[0].shape[2] if V is None else V
+    dev = models[0].device
+    npair = N * (N - 1) // 2
+    desc = (msd_logits * N)(*[logits_desc(t) for t in models])
+    out = dict(pos_dtv=torch.zeros((npair, B, K), dtype=torch.float32, device=dev),
+               pos_kl=torch.zeros((npair, B, K), dtype=torch.float32, device=dev),
+               flags=torch.zeros((B,), dtype=torch.int32, device=dev))
+    if stats:
+        out["stats"] = torch.zeros((npair, len(STATS_FIELDS)), dtype=torch.int64, device=dev)
+    st = lib().msd_pool_divergence(desc, N, B, K, V, _ptr(out["pos_dtv"]), _ptr(out["pos_kl"]),
+                                   _ptr(out.get("stats")), _ptr(out["flags"]), _stream(stream))
+    _check(st, "msd_pool_divergence")
+    return out
 
 
 # ------------------------------------------------------------------ scheduler feed (host C)

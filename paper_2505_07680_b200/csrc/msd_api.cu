@@ -334,6 +334,34 @@ msd_status msd_kv_rollback(const msd_paged_kv* kv, int32_t n_models, int32_t B,
     return MSD_OK;
 }
 
+msd_status msd_pool_divergence(const msd_logits* models, int32_t N, int32_t B, int32_t K, int64_t V,
+                               float* pos_dtv, float* pos_kl, msd_pair_stats* stats, uint32_t* flags,
+                               void* stream) {
+    if (!models) return fail(MSD_E_ARG, "models is NULL");
+    if (N < 2 || N > 4) return fail(MSD_E_ARG, "N=%d outside [2,4]", N);
+    if (B < 0 || K < 1) return fail(MSD_E_ARG, "bad B=%d / K=%d", B, K);
+    if (V < 1) return fail(MSD_E_ARG, "V=%lld < 1", (long long)V);
+    if (B == 0) return MSD_OK;
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    int32_t bf16 = 0;
+    st = validate_levels(models, N, K, V, 0, 0, &bf16);   // every model needs >= K rows
+    if (st != MSD_OK) return st;
+    PoolParams pp;
+    memset(&pp, 0, sizeof(pp));
+    for (int l = 0; l < N; ++l) {
+        pp.lv.ptr[l] = models[l].ptr;
+        pp.lv.ld[l] = models[l].ld;
+        pp.lv.bs[l] = models[l].batch_stride;
+        pp.lv.rows[l] = models[l].rows;
+    }
+    pp.N = N; pp.B = B; pp.K = K; pp.V = V;
+    pp.pos_dtv = pos_dtv; pp.pos_kl = pos_kl; pp.stats = stats; pp.flags = flags;
+    cudaError_t e = launch_pool(pp, bf16, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "msd_pool launch");
+    return MSD_OK;
+}
+
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes) {
     g_trace = reinterpret_cast<unsigned long long*>(dev_buf);
     g_trace_items = dev_buf ? bytes / 128 : 0;

@@ -77,6 +77,16 @@ struct TailParams {
     const double* exptab;   // exp of every bf16 value (exact-draw path), from exp_table()
 };
 
+struct PoolParams {          // SimScore bootstrap (msd_pool.cu)
+    LevelDesc lv;
+    int32_t N, B, K;
+    int64_t V;
+    float* pos_dtv;
+    float* pos_kl;
+    msd_pair_stats* stats;
+    uint32_t* flags;
+};
+
 struct RollbackParams {
     msd_paged_kv kv[8];
     int32_t n_models, B;
@@ -88,5 +98,6 @@ struct RollbackParams {
 cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s);
 cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_rollback(const RollbackParams& p, cudaStream_t s);
+cudaError_t launch_pool(const PoolParams& p, int bf16, cudaStream_t s);
 
 }  // namespace msd

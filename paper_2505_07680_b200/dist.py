@@ -56,36 +56,60 @@ def allreduce_stats(stats: torch.Tensor) -> torch.Tensor:
 
 @dataclass
 class ChainScheduler:
-    """Host scheduler fed by the reduced per-pair stats (row a8).
+    """Host scheduler fed by the reduced per-pair stats (row a8) over a pool of P models.
 
-    sim[l]: EMA of SimScore = 1 - mean DTV of the adjacent pair (M_l, M_{l+1}) (Eq. 6,
-    weight `ema`, R13); alpha = SimScore (R11); the chain is Alg. 1's argmin of
-    Eq. 7's T_eff over the chains through the L models that end at the target.
+    sim: P x P SimScores (EMA of 1 - mean DTV, Eq. 6, weight `ema`, R13); alpha =
+    SimScore (R11).  `bootstrap` initialises every pair from msd_pool_divergence stats
+    (observation count 1); `update` folds one step's stats of the running chain's
+    adjacent pairs into their SimScores; the next chain is Alg. 1's argmin of Eq. 7's T_eff
+    over every chain of the pool that ends at the target.  Without a bootstrap a
+    pair's SimScore starts at the `prior` (0.5) until the chain first runs it.
     """
     T_ms: list
     W: int
     ema: float = 0.1
     max_len: int = 4
-    sim: list = field(default_factory=list)
-    first: bool = True
+    prior: float = 0.5
+    sim: list = field(default_factory=list)          # P x P
+    seen: list = field(default_factory=list)         # P x P: pair has an observation
     chain: list = field(default_factory=list)
     t_eff: float | None = None
 
     def __post_init__(self):
         P = len(self.T_ms)
         if not self.sim:
-            self.sim = [0.5] * (P - 1)
+            self.sim = [[1.0 if i == j else self.prior for j in range(P)] for i in range(P)]
+        if not self.seen:
+            self.seen = [[i == j for j in range(P)] for i in range(P)]
         if not self.chain:
             self.chain = list(range(P))
 
-    def update(self, stats_rows) -> list:
-        """stats_rows: [L-1][8] int64 totals (all ranks identical after allreduce_stats)."""
+    def _fold(self, i, j, stats_row):
+        first = not self.seen[i][j]
+        v = api.simscore_update(self.sim[i][j], stats_row, self.ema, first)
+        self.sim[i][j] = self.sim[j][i] = v
+        self.seen[i][j] = self.seen[j][i] = True
+
+    def bootstrap(self, pool_stats) -> list:
+        """pool_stats: [P(P-1)/2][8] int64 totals of msd_pool_divergence (pairs i < j in
+        lexicographic order, all ranks identical after allreduce_stats)."""
         P = len(self.T_ms)
-        for l in range(P - 1):
-            self.sim[l] = api.simscore_update(self.sim[l], stats_rows[l], self.ema, self.first)
-        self.first = False
-        sim = [[0.0] * P for _ in range(P)]
-        for l in range(P - 1):
-            sim[l][l + 1] = self.sim[l]
-        self.chain, self.t_eff = api.select_chain(self.T_ms, sim, self.W, max_len=self.max_len)
+        q = 0
+        for i in range(P):
+            for j in range(i + 1, P):
+                self.seen[i][j] = self.seen[j][i] = False
+                self._fold(i, j, pool_stats[q])
+                q += 1
+        return self._select()
+
+    def update(self, stats_rows, chain=None) -> list:
+        """stats_rows: [len(chain)-1][8] int64 totals of the adjacent pairs of the chain that
+        ran (default: the last selected chain)."""
+        ran = list(self.chain if chain is None else chain)
+        for l in range(len(ran) - 1):
+            self._fold(ran[l], ran[l + 1], stats_rows[l])
+        return self._select()
+
+    def _select(self) -> list:
+        self.chain, self.t_eff = api.select_chain(self.T_ms, self.sim, self.W, max_len=self.max_len)
         return self.chain

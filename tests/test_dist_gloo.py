@@ -124,7 +124,7 @@ def test_scheduler_decision_matches_single_process(two_ranks):
     assert math.isclose(sch.t_eff, t0, rel_tol=0, abs_tol=0)
     # SimScore = 1 - mean DTV of each adjacent pair (Eq. 6), first update takes the observation
     for l in range(L - 1):
-        assert math.isclose(sch.sim[l], 1.0 - single[l, 0] / (DTV_SCALE * single[l, 2]), rel_tol=1e-12)
+        assert math.isclose(sch.sim[l][l + 1], 1.0 - single[l, 0] / (DTV_SCALE * single[l, 2]), rel_tol=1e-12)
 
 
 def test_allreduce_rejects_non_integer_stats():
