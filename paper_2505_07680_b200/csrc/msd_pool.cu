@@ -16,6 +16,7 @@ namespace msd {
 
 constexpr int PT = 256;           // threads per CTA
 constexpr int PNW = PT / 32;
+constexpr int UNR = 2;            // vectors per row in flight per thread
 
 template <typename Tin>
 __device__ __forceinline__ void pool_vec(const Tin* row, int64_t e, int64_t V, float* x) {
@@ -28,8 +29,91 @@ __device__ __forceinline__ void pool_vec(const Tin* row, int64_t e, int64_t V, f
     }
 }
 
+
+template <int N, int VEC>
+__device__ __forceinline__ void p1_accum(const float (&x)[N][VEC], float (&m)[N], double (&S)[N]) {
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+        float mv = x[l][0];
+#pragma unroll
+        for (int q = 1; q < VEC; ++q) mv = max_nan_f32(mv, x[l][q]);
+        if (!(mv <= m[l])) {                         // larger (or NaN): rescale the running sum
+            S[l] = (m[l] == -INFINITY) ? 0.0 : S[l] * dexp_neg((double)m[l] - (double)mv);
+            m[l] = mv;
+        }
+        float sv = 0.f;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) sv += ex2f((x[l][q] - m[l]) * LOG2E);
+        S[l] += (double)sv;
+    }
+}
+
+// y_l = z_l - LSE_l, p_l = 2^(y_l log2 e); per pair (i < j): sum |p_j - p_i| and
+// sum_{p_j > 0} p_j (y_j - y_i)  (fp32 per vector, float64 sums)
+template <int N, int VEC, int NP>
+__device__ __forceinline__ void p2_accum(const float (&x)[N][VEC], const float (&Lh)[N],
+                                         const float (&Ll)[N], double (&dacc)[NP],
+                                         double (&kacc)[NP], int& kinf) {
+    float y[N][VEC], pr[N][VEC];
+#pragma unroll
+    for (int l = 0; l < N; ++l)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+            y[l][q] = (x[l][q] > NEG_MASKED) ? (x[l][q] - Lh[l]) - Ll[l] : -INFINITY;
+            pr[l][q] = ex2f(y[l][q] * LOG2E);
+        }
+    int pi = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+#pragma unroll
+        for (int j = i + 1; j < N; ++j, ++pi) {
+            float dv = 0.f, kv = 0.f;
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+                dv += fabsf(pr[j][q] - pr[i][q]);
+                if (y[j][q] > -INFINITY) {              // p_j > 0 (a finite logit; 0 log 0 = 0)
+                    if (y[i][q] == -INFINITY) kinf |= 1 << pi;
+                    else kv = fmaf(pr[j][q], y[j][q] - y[i][q], kv);
+                }
+            }
+            dacc[pi] += (double)dv;
+            kacc[pi] += (double)kv;
+        }
+    }
+}
+
+template <typename Tin, int N, typename F>
+__device__ __forceinline__ void pool_stream(const Tin* const (&rows)[N], int64_t V, int tid, F&& f) {
+    // UNR full vectors per row per iteration, every load issued before any arithmetic (bytes in
+    // flight); then the ragged remainder one vector at a time
+    constexpr int VEC = Elem<Tin>::VEC;
+    constexpr int64_t STEP = (int64_t)PT * VEC;
+    int64_t e0 = (int64_t)tid * VEC;
+    for (; e0 + (UNR - 1) * STEP + VEC <= V; e0 += UNR * STEP) {
+        uint4 raw[UNR][N];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int l = 0; l < N; ++l)
+                raw[u][l] = __ldg(reinterpret_cast<const uint4*>(rows[l] + e0 + u * STEP));
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            float x[N][VEC];
+#pragma unroll
+            for (int l = 0; l < N; ++l) unpack_clamped<Tin>(raw[u][l], x[l]);
+            f(x);
+        }
+    }
+    for (; e0 < V; e0 += STEP) {
+        float x[N][VEC];
+#pragma unroll
+        for (int l = 0; l < N; ++l) pool_vec<Tin>(rows[l], e0, V, x[l]);
+        f(x);
+    }
+}
+
 template <typename Tin, int N>
-__global__ void __launch_bounds__(PT) pool_kernel(PoolParams p) {
+__global__ void __launch_bounds__(PT, 2) pool_kernel(PoolParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NP = N * (N - 1) / 2;
     const int64_t pos = blockIdx.x;                 // b * K + k
@@ -40,7 +124,7 @@ __global__ void __launch_bounds__(PT) pool_kernel(PoolParams p) {
     __shared__ float redm[N][PNW];
     __shared__ double lse_s[N];
     __shared__ int bad_s[N];
-    const Tin* rows[N];
+    const Tin* rows[N];  // row (b, k) of every model
 #pragma unroll
     for (int l = 0; l < N; ++l)
         rows[l] = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] + k * p.lv.ld[l];
@@ -50,24 +134,7 @@ __global__ void __launch_bounds__(PT) pool_kernel(PoolParams p) {
     double S[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) { m[l] = -INFINITY; S[l] = 0.0; }
-    for (int64_t e = (int64_t)tid * VEC; e < V; e += (int64_t)PT * VEC) {
-#pragma unroll
-        for (int l = 0; l < N; ++l) {
-            float x[VEC];
-            pool_vec<Tin>(rows[l], e, V, x);
-            float mv = x[0];
-#pragma unroll
-            for (int q = 1; q < VEC; ++q) mv = max_nan_f32(mv, x[q]);
-            if (!(mv <= m[l])) {                     // larger (or NaN): rescale the running sum
-                S[l] = (m[l] == -INFINITY) ? 0.0 : S[l] * dexp_neg((double)m[l] - (double)mv);
-                m[l] = mv;
-            }
-            float sv = 0.f;
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) sv += ex2f((x[q] - m[l]) * LOG2E);
-            S[l] += (double)sv;
-        }
-    }
+    pool_stream<Tin, N>(rows, V, tid, [&](const float (&x)[N][VEC]) { p1_accum<N, VEC>(x, m, S); });
 #pragma unroll
     for (int l = 0; l < N; ++l) {
         const float wm = warp_max(m[l]);
@@ -94,43 +161,14 @@ __global__ void __launch_bounds__(PT) pool_kernel(PoolParams p) {
         Ll[l] = (float)(lse_s[l] - (double)Lh[l]);
     }
 
-    // ---- pass 2: every pair at once.  y_l = z_l - LSE_l, p_l = 2^(y_l log2 e); per pair
-    // (i < j): sum |p_j - p_i| and sum_{p_j > 0} p_j (y_j - y_i)  (fp32 per vector, float64 sums)
+    // ---- pass 2: every pair at once (p2_accum)
     double dacc[NP], kacc[NP];
     int kinf = 0;
 #pragma unroll
     for (int q = 0; q < NP; ++q) { dacc[q] = 0.0; kacc[q] = 0.0; }
-    for (int64_t e = (int64_t)tid * VEC; e < V; e += (int64_t)PT * VEC) {
-        float y[N][VEC], pr[N][VEC];
-#pragma unroll
-        for (int l = 0; l < N; ++l) {
-            float x[VEC];
-            pool_vec<Tin>(rows[l], e, V, x);
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-                y[l][q] = (x[q] > NEG_MASKED) ? (x[q] - Lh[l]) - Ll[l] : -INFINITY;
-                pr[l][q] = ex2f(y[l][q] * LOG2E);
-            }
-        }
-        int pi = 0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-#pragma unroll
-            for (int j = i + 1; j < N; ++j, ++pi) {
-                float dv = 0.f, kv = 0.f;
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) {
-                    dv += fabsf(pr[j][q] - pr[i][q]);
-                    if (y[j][q] > -INFINITY) {          // p_j > 0 (a finite logit; 0 log 0 = 0)
-                        if (y[i][q] == -INFINITY) kinf |= 1 << pi;
-                        else kv = fmaf(pr[j][q], y[j][q] - y[i][q], kv);
-                    }
-                }
-                dacc[pi] += (double)dv;
-                kacc[pi] += (double)kv;
-            }
-        }
-    }
+    pool_stream<Tin, N>(rows, V, tid, [&](const float (&x)[N][VEC]) {
+        p2_accum<N, VEC, NP>(x, Lh, Ll, dacc, kacc, kinf);
+    });
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         const double d = warp_sum_d(dacc[q]), kk = warp_sum_d(kacc[q]);
