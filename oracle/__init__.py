@@ -69,6 +69,8 @@ def lib() -> ctypes.CDLL:
         L.or_select_chain.argtypes = [i32, P, P, i32, i32, i32, i32, P, P]
         L.or_pool_divergence.restype = None
         L.or_pool_divergence.argtypes = [P, i32, i32, i32, i64, P, P]
+        L.or_draft_sample.restype = None
+        L.or_draft_sample.argtypes = [P, i64, i32, i64, P, i32, d, P, P, P, P]
         _ = u32
         _lib = L
     return _lib
@@ -280,3 +282,16 @@ def bootstrap_sim(levels):
             sim[i, j] = sim[j, i] = 1.0 - float(dtv[pi].mean())
             pi += 1
     return sim
+
+
+def draft_sample(z, u, greedy=False, tie_eps_draw=1e-7):
+    """Draft-side sampling step: z [B][V] drafter logits,
+    u [B] uniforms -> dict(token int32 [B], lse, q_tok float64 [B], near_tie int32 [B])."""
+    z = _f64(z)
+    B, V = z.shape
+    u = np.ascontiguousarray(u, dtype=np.float32)
+    out = dict(token=np.zeros(B, np.int32), lse=np.zeros(B), q_tok=np.zeros(B),
+               near_tie=np.zeros(B, np.int32))
+    lib().or_draft_sample(_p(z), V, B, V, _p(u), int(bool(greedy)), tie_eps_draw,
+                          _p(out["token"]), _p(out["lse"]), _p(out["q_tok"]), _p(out["near_tie"]))
+    return out

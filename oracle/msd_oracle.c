@@ -482,3 +482,28 @@ void or_pool_divergence(const or_level* lv, int32_t N, int32_t B, int32_t K, int
         (void)np;
     }
 }
+
+/* Draft-side sampling, one draft step for B sequences ("the draft
+ * model ... autoregressively generates a sequence of gamma candidate tokens"
+ * DraftProcessor; "W sequential next_dist+sample (or argmax in greedy mode)"):
+ * row b of z is the drafter's logits for the next token.  token[b] = or_sample (inverse CDF
+ * of softmax(z_b) with u[b], reading R5) or or_argmax in greedy mode; lse[b] = log sum exp
+ * z_b (Eq. 1); q_tok[b] = softmax(z_b)[token[b]] (the q(x) the verifier's ratio needs).
+ * A row whose LSE is not finite (every entry -inf, a NaN, or +inf) gives token -1. */
+void or_draft_sample(const double* z, int64_t ld, int32_t B, int64_t V, const float* u,
+                     int32_t greedy, double tie_eps_draw, int32_t* token, double* lse,
+                     double* q_tok, int32_t* near_tie) {
+    g_tie_eps_draw = tie_eps_draw;
+#pragma omp parallel for schedule(dynamic)
+    for (int32_t b = 0; b < B; ++b) {
+        const double* zb = z + (int64_t)b * ld;
+        const double A = or_lse(zb, V);
+        int nt = 0;
+        int64_t t = -1;
+        if (isfinite(A)) t = greedy ? or_argmax(zb, V) : or_sample(zb, A, V, (double)u[b], &nt);
+        token[b] = (int32_t)t;
+        lse[b] = A;
+        q_tok[b] = t >= 0 ? exp(zb[t] - A) : NAN;
+        near_tie[b] = nt;
+    }
+}

@@ -103,6 +103,14 @@ int32_t or_select_chain(int32_t P, const double* T, const double* sim, int32_t W
 void or_pool_divergence(const or_level* lv, int32_t N, int32_t B, int32_t K, int64_t V,
                         double* dtv, double* kl);
 
+/* Draft-side sampling: one draft step for B
+ * rows z[b * ld + v]: token = inverse-CDF draw from softmax (u[b]) or argmax (greedy), lse,
+ * q_tok = softmax(z_b)[token], near_tie = |u - C/Z| < tie_eps_draw at the drawn token's CDF
+ * boundaries.  Non-finite LSE -> token -1.  Pinned by tests/test_oracle_draft.py. */
+void or_draft_sample(const double* z, int64_t ld, int32_t B, int64_t V, const float* u,
+                     int32_t greedy, double tie_eps_draw, int32_t* token, double* lse,
+                     double* q_tok, int32_t* near_tie);
+
 #ifdef __cplusplus
 }
 #endif
