@@ -238,6 +238,28 @@ msd_status msd_pool_divergence(const msd_logits* models, int32_t N, int32_t B, i
                                void* stream);
 
 /* ---------------------------------------------------------------------------
+ * msd_draft_sample -- one draft-side sampling step for B sequences (
+ *    P:62 "the draft model ... autoregressively generates ... gamma candidate tokens",
+ *    P:245 DraftProcessor; "W sequential next_dist+sample (or argmax in greedy
+ *    mode)").  Called once per draft step k (the drafter's forward is the caller's).
+ *
+ * drafter (HOST pointer to one descriptor): logits [B][rows][ld]; row `row` (0 <= row <
+ *    rows) of every request is sampled; V <= ld, 16-byte aligned rows, V <= 2^21.
+ * u[B] (device f32 in [0,1)): the uniforms, ignored when greedy.
+ * token[B] (device int32, required): min{t : C_t > u Z}, C_t = sum_{v<=t} exp(z_v - M),
+ *    Z = C_{V-1} (inverse CDF of softmax, reading R5; tokens with p = 0 are never drawn);
+ *    greedy: the first argmax.  -1 for a row without a finite LSE (NONFINITE flag).
+ * lse[B] (device f32, NULL ok): log sum_v exp z_v (Eq. 1).
+ * q_tok[B] (device f32, NULL ok): softmax(z)[token] -- the q(x) of the acceptance ratio.
+ * flags[B] (device, NULL ok): |= NONFINITE; NEAR_TIE when u Z is within 1e-6 Z of the drawn
+ *    token's CDF boundaries (float64 rescan; the decision can differ from exact arithmetic
+ *    only there).  Asynchronous on `stream`; no workspace; one read of each row.
+ * ------------------------------------------------------------------------- */
+msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, int64_t V,
+                            const float* u, int32_t greedy, int32_t* token, float* lse,
+                            float* q_tok, uint32_t* flags, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics.
  * msd_last_error: thread-local message for the last non-OK status of this thread.
  * msd_prof_enable(1): record CUDA events around every msd_core launch (the

@@ -78,6 +78,8 @@ def lib() -> ctypes.CDLL:
     L.msd_kv_rollback.argtypes = [P, i32, i32, P, P, P]
     L.msd_pool_divergence.restype = i32
     L.msd_pool_divergence.argtypes = [P, i32, i32, i32, i64, P, P, P, P, P]
+    L.msd_draft_sample.restype = i32
+    L.msd_draft_sample.argtypes = [P, i32, i32, i64, P, i32, P, P, P, P, P]
     L.msd_predict_chain_latency.restype = i32
     L.msd_predict_chain_latency.argtypes = [i32, P, P, i32, i32, i32, P]
     L.msd_select_chain.restype = i32
@@ -271,6 +273,27 @@ def pool_divergence(models: Sequence[torch.Tensor], K: Optional[int] = None, V: 
     st = lib().msd_pool_divergence(desc, N, B, K, V, _ptr(out["pos_dtv"]), _ptr(out["pos_kl"]),
                                    _ptr(out.get("stats")), _ptr(out["flags"]), _stream(stream))
     _check(st, "msd_pool_divergence")
+    return out
+
+
+def draft_sample(drafter: torch.Tensor, u: Optional[torch.Tensor], row: int = 0, V: Optional[int] = None,
+                 greedy: bool = False, out: Optional[dict] = None, stream=None) -> dict:
+    """msd_draft_sample: one draft-side sampling step.
+    drafter: [B][rows][ld] logits (row `row` is sampled); u: [B] f32 uniforms (None if greedy).
+    Returns device tensors token int32 [B], lse / q_tok f32 [B], flags [B] (`out` reuses them)."""
+    B = drafter.shape[0]
+    V = drafter.shape[2] if V is None else V
+    dev = drafter.device
+    if out is None:
+        out = dict(token=torch.empty((B,), dtype=torch.int32, device=dev),
+                   lse=torch.empty((B,), dtype=torch.float32, device=dev),
+                   q_tok=torch.empty((B,), dtype=torch.float32, device=dev),
+                   flags=torch.zeros((B,), dtype=torch.int32, device=dev))
+    d = logits_desc(drafter)
+    st = lib().msd_draft_sample(ctypes.byref(d), int(row), B, V, _ptr(u), int(bool(greedy)),
+                                _ptr(out["token"]), _ptr(out["lse"]), _ptr(out["q_tok"]),
+                                _ptr(out["flags"]), _stream(stream))
+    _check(st, "msd_draft_sample")
     return out
 
 

@@ -362,6 +362,31 @@ msd_status msd_pool_divergence(const msd_logits* models, int32_t N, int32_t B, i
     return MSD_OK;
 }
 
+msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, int64_t V,
+                            const float* u, int32_t greedy, int32_t* token, float* lse,
+                            float* q_tok, uint32_t* flags, void* stream) {
+    if (!drafter) return fail(MSD_E_ARG, "drafter is NULL");
+    if (B < 0) return fail(MSD_E_ARG, "B=%d < 0", B);
+    if (V < 1 || V > (1 << 21)) return fail(MSD_E_ARG, "V=%lld outside [1, 2^21]", (long long)V);
+    if (row < 0 || row >= drafter->rows) return fail(MSD_E_ARG, "row=%d outside [0, rows=%d)", row, drafter->rows);
+    if (B == 0) return MSD_OK;
+    if (!token) return fail(MSD_E_ARG, "token is NULL");
+    if (!greedy && !u) return fail(MSD_E_ARG, "u is NULL (stochastic mode)");
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    int32_t bf16 = 0;
+    st = validate_levels(drafter, 1, row + 1, V, 0, 0, &bf16);
+    if (st != MSD_OK) return st;
+    DraftParams dp;
+    memset(&dp, 0, sizeof(dp));
+    dp.z = drafter->ptr; dp.ld = drafter->ld; dp.bs = drafter->batch_stride;
+    dp.row = row; dp.B = B; dp.greedy = greedy ? 1 : 0; dp.V = V;
+    dp.u = u; dp.token = token; dp.lse = lse; dp.q_tok = q_tok; dp.flags = flags;
+    cudaError_t e = launch_draft(dp, bf16, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "msd_draft launch");
+    return MSD_OK;
+}
+
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes) {
     g_trace = reinterpret_cast<unsigned long long*>(dev_buf);
     g_trace_items = dev_buf ? bytes / 128 : 0;

@@ -87,6 +87,18 @@ struct PoolParams {          // SimScore bootstrap (msd_pool.cu)
     uint32_t* flags;
 };
 
+struct DraftParams {         // draft-side sampling step (msd_draft.cu)
+    const void* z;
+    int64_t ld, bs;
+    int32_t row, B, greedy;
+    int64_t V;
+    const float* u;
+    int32_t* token;
+    float* lse;
+    float* q_tok;
+    uint32_t* flags;
+};
+
 struct RollbackParams {
     msd_paged_kv kv[8];
     int32_t n_models, B;
@@ -99,5 +111,6 @@ cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t 
 cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_rollback(const RollbackParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int bf16, cudaStream_t s);
+cudaError_t launch_draft(const DraftParams& p, int bf16, cudaStream_t s);
 
 }  // namespace msd
