@@ -244,7 +244,7 @@ msd_status msd_pool_divergence(const msd_logits* models, int32_t N, int32_t B, i
  *    mode)").  Called once per draft step k (the drafter's forward is the caller's).
  *
  * drafter (HOST pointer to one descriptor): logits [B][rows][ld]; row `row` (0 <= row <
- *    rows) of every request is sampled; V <= ld, 16-byte aligned rows, V <= 2^21.
+ *    rows) of every request is sampled; V <= ld, 16-byte aligned rows, V <= 2^18.
  * u[B] (device f32 in [0,1)): the uniforms, ignored when greedy.
  * token[B] (device int32, required): min{t : C_t > u Z}, C_t = sum_{v<=t} exp(z_v - M),
  *    Z = C_{V-1} (inverse CDF of softmax, reading R5; tokens with p = 0 are never drawn);

@@ -367,7 +367,7 @@ msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, i
                             float* q_tok, uint32_t* flags, void* stream) {
     if (!drafter) return fail(MSD_E_ARG, "drafter is NULL");
     if (B < 0) return fail(MSD_E_ARG, "B=%d < 0", B);
-    if (V < 1 || V > (1 << 21)) return fail(MSD_E_ARG, "V=%lld outside [1, 2^21]", (long long)V);
+    if (V < 1 || V > (1 << 18)) return fail(MSD_E_ARG, "V=%lld outside [1, 2^18]", (long long)V);
     if (row < 0 || row >= drafter->rows) return fail(MSD_E_ARG, "row=%d outside [0, rows=%d)", row, drafter->rows);
     if (B == 0) return MSD_OK;
     if (!token) return fail(MSD_E_ARG, "token is NULL");

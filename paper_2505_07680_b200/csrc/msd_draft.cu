@@ -11,8 +11,9 @@
 // 32 * VEC consecutive entries and leaves its (chunk max, fp64 chunk sum) in shared memory;
 // the CTA then combines the chunks in float64, finds the chunk holding the crossing by a
 // block-wide fp64 prefix, and one warp rescans that chunk (from L1/L2, 512 B) with float64
-// weights exp(z - M) to place the token.  The exponentials of the streaming pass are split
-// between MUFU ex2 and an FMA-pipe polynomial (MUFU alone would bound the kernel above HBM).
+// weights exp(z - M) to place the token.  bf16 rows are reduced straight from the loaded
+// words with packed f32x2 arithmetic; 2 of every 8 exponentials run as an FMA-pipe
+// polynomial (MUFU alone would bound the kernel above HBM time).
 #include "msd_common.cuh"
 #include "msd_internal.h"
 
@@ -20,7 +21,6 @@ namespace msd {
 
 constexpr int DT = 256;                 // threads per CTA
 constexpr int DNW = DT / 32;
-constexpr int DCV = 4;                  // vectors per lane per chunk (chunk = 32 * DCV * VEC entries)
 
 template <typename Tin>
 __device__ __forceinline__ void draft_vec(const Tin* row, int64_t e, int64_t V, float* x) {
@@ -51,10 +51,17 @@ __device__ __forceinline__ float warp_max_nan(float v) {
     return v;
 }
 
-// one chunk held in registers: CV vectors per lane -> (warp max, float64 warp sum)
+__device__ __forceinline__ float redux_max_nan_f32(float v) {
+    float r;
+    asm("redux.sync.max.NaN.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
+
+// one chunk held in registers: CV vectors per lane -> warp max (one redux) and this lane's
+// fp32 partial sum of exp(x - warp max); the float64 warp sums are formed after the stream
 template <typename Tin, int CV, bool GREEDY>
 __device__ __forceinline__ void chunk_stats(const float (&x)[CV][Elem<Tin>::VEC], int64_t e0,
-                                            float& bestv, int& besti, float& wm, double& ws) {
+                                            float& bestv, int& besti, float& wm, float& ls) {
     constexpr int VEC = Elem<Tin>::VEC;
     float mv = x[0][0];
 #pragma unroll
@@ -68,17 +75,78 @@ __device__ __forceinline__ void chunk_stats(const float (&x)[CV][Elem<Tin>::VEC]
             for (int q = 0; q < VEC; ++q)
                 if (x[v][q] > bestv) { bestv = x[v][q]; besti = (int)(e0 + v * 32 * VEC) + q; }
     }
-    wm = warp_max_nan(mv);
-    double s = 0.0;
+    wm = redux_max_nan_f32(mv);
+    float s = 0.f;
     if (wm > NEG_MASKED) {
 #pragma unroll
-        for (int v = 0; v < CV; ++v) s += (double)vec_expsum<VEC>(x[v], wm);
+        for (int v = 0; v < CV; ++v) s += vec_expsum<VEC>(x[v], wm);
     }
-    ws = warp_sum_d(s);
+    ls = s;
 }
 
-template <typename Tin, bool GREEDY>
-__global__ void __launch_bounds__(DT, 4) draft_kernel(DraftParams p) {
+// 2^x for a pair of x <= 0 on the FMA pipe with packed f32x2 ops, branch-free: x clamped at
+// -127 (-> exactly 0, like ex2.approx.ftz), n = rint(x) by the 1.5*2^23 magic, degree-6
+// Taylor polynomial of e^(t), t = (x - n) ln 2, |t| <= 0.347 (truncation 1.2e-7 relative).
+__device__ __forceinline__ float2 exp2_pair_fma(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 xm = __fadd2_rn(x, magic);
+    const float2 n = __fadd2_rn(xm, make_float2(-12582912.f, -12582912.f));
+    const float2 ln2 = make_float2(0.69314718056f, 0.69314718056f);
+    const float2 t = __fmul2_rn(__fadd2_rn(x, make_float2(-n.x, -n.y)), ln2);
+    float2 r = make_float2(1.38888889e-3f, 1.38888889e-3f);                  // 1/6!
+    r = __ffma2_rn(r, t, make_float2(8.33333333e-3f, 8.33333333e-3f));
+    r = __ffma2_rn(r, t, make_float2(4.16666667e-2f, 4.16666667e-2f));
+    r = __ffma2_rn(r, t, make_float2(1.66666667e-1f, 1.66666667e-1f));
+    r = __ffma2_rn(r, t, make_float2(0.5f, 0.5f));
+    r = __ffma2_rn(r, t, make_float2(1.0f, 1.0f));
+    r = __ffma2_rn(r, t, make_float2(1.0f, 1.0f));
+    const int nx = __float_as_int(xm.x) - 0x4B400000, ny = __float_as_int(xm.y) - 0x4B400000;
+    return __fmul2_rn(r, make_float2(__int_as_float((nx + 127) << 23), __int_as_float((ny + 127) << 23)));
+}
+
+// bf16 chunk straight from the loaded words: max.NaN.bf16x2 for the lane maximum, then per
+// pair FHADD.BF16 (x - wm without unpacking), one FMUL2 by log2 e, ex2 (every 8th element on
+// the FMA pipe) and FADD2 partial sums -- about 3.5 issue slots per element.  Same values
+// as chunk_stats on unpacked floats: x - wm and (x - wm) log2 e round identically.
+template <int CV, int NPOLY>
+__device__ __forceinline__ void chunk_stats_bf16(const uint4 (&raw)[CV], float& wm, float& ls) {
+    uint32_t mw = raw[0].x;
+#pragma unroll
+    for (int v = 0; v < CV; ++v) {
+        mw = max_nan_bf16x2(mw, raw[v].x);
+        mw = max_nan_bf16x2(mw, raw[v].y);
+        mw = max_nan_bf16x2(mw, raw[v].z);
+        mw = max_nan_bf16x2(mw, raw[v].w);
+    }
+    wm = redux_max_nan_f32(max_nan_f32(bf16lo(mw), bf16hi(mw)));
+    float2 acc = make_float2(0.f, 0.f);
+    if (wm > NEG_MASKED) {
+        const float nm = -wm;
+        const float2 l2e = make_float2(LOG2E, LOG2E);
+#pragma unroll
+        for (int v = 0; v < CV; ++v) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t w = k == 0 ? raw[v].x : k == 1 ? raw[v].y : k == 2 ? raw[v].z : raw[v].w;
+                float2 y;
+                asm("{ .reg .b16 lo, hi; mov.b32 {lo, hi}, %2; add.rn.f32.bf16 %0, lo, %3; add.rn.f32.bf16 %1, hi, %3; }"
+                    : "=f"(y.x), "=f"(y.y) : "r"(w), "f"(nm));
+                const float2 t = __fmul2_rn(y, l2e);
+                float2 e;
+                if (2 * k >= 8 - NPOLY) e = exp2_pair_fma(t);      // NPOLY even: whole pairs
+                else { e.x = ex2f(t.x); e.y = ex2f(t.y); }
+                acc = __fadd2_rn(acc, e);
+            }
+        }
+    }
+    ls = acc.x + acc.y;
+}
+
+template <typename Tin, bool GREEDY, int DCV, int MINB, int DNPOLY>
+__global__ void __launch_bounds__(DT, MINB) draft_kernel(DraftParams p) {
+    // DCV vectors per lane per chunk (chunk = 32 * DCV * VEC entries)
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int SB = 32 * VEC;                          // entries per warp-vector (sub-block)
     constexpr int CH = DCV * SB;                          // entries per chunk
@@ -86,6 +154,7 @@ __global__ void __launch_bounds__(DT, 4) draft_kernel(DraftParams p) {
     const int nch = (int)ceil_div(p.V, CH);
     float* cmax = reinterpret_cast<float*>(dsm);                       // [nch]
     double* csum = reinterpret_cast<double*>(dsm + align_up((size_t)nch * 4, 16));   // [nch]
+    float* lsum = reinterpret_cast<float*>(csum + nch);                 // [nch][32] lane partials
     __shared__ double wred[DNW];
     __shared__ float fred[DNW];
     __shared__ int ired[DNW];
@@ -104,26 +173,51 @@ __global__ void __launch_bounds__(DT, 4) draft_kernel(DraftParams p) {
     float bestv = -INFINITY;
     int besti = INT_MAX;
     const int nfull = (int)(V / CH);                       // chunks entirely inside the row
-    uint4 raw[DCV];
     int c = warp;
-    if (c < nfull) {
-#pragma unroll
-        for (int v = 0; v < DCV; ++v)
-            raw[v] = __ldg(reinterpret_cast<const uint4*>(row + (int64_t)c * CH + (v * 32 + lane) * VEC));
-    }
-    for (; c < nfull; c += DNW) {
-        float x[DCV][VEC];
-#pragma unroll
-        for (int v = 0; v < DCV; ++v) unpack_clamped<Tin>(raw[v], x[v]);
-        if (c + DNW < nfull) {
+    if (sizeof(Tin) == 2 && !GREEDY) {
+        // bf16: two register buffers, chunk c + 8 loads while chunk c is reduced
+        uint4 ra[DCV], rb[DCV];
+        auto ld = [&](uint4 (&r)[DCV], int cc) {
 #pragma unroll
             for (int v = 0; v < DCV; ++v)
-                raw[v] = __ldg(reinterpret_cast<const uint4*>(row + (int64_t)(c + DNW) * CH + (v * 32 + lane) * VEC));
+                r[v] = __ldg(reinterpret_cast<const uint4*>(row + (int64_t)cc * CH + (v * 32 + lane) * VEC));
+        };
+        auto put = [&](int cc, float wm, float ls) {
+            lsum[cc * 32 + lane] = ls;
+            if (lane == 0) cmax[cc] = wm;
+        };
+        if (c < nfull) ld(ra, c);
+        for (; c < nfull; c += 2 * DNW) {
+            float wm, ls;
+            if (c + DNW < nfull) ld(rb, c + DNW);
+            chunk_stats_bf16<DCV, DNPOLY>(ra, wm, ls);
+            put(c, wm, ls);
+            if (c + DNW >= nfull) break;
+            if (c + 2 * DNW < nfull) ld(ra, c + 2 * DNW);
+            chunk_stats_bf16<DCV, DNPOLY>(rb, wm, ls);
+            put(c + DNW, wm, ls);
         }
-        float wm;
-        double ws;
-        chunk_stats<Tin, DCV, GREEDY>(x, (int64_t)c * CH + lane * VEC, bestv, besti, wm, ws);
-        if (lane == 0) { cmax[c] = wm; csum[c] = ws; }
+    } else {
+        uint4 raw[DCV];
+        if (c < nfull) {
+#pragma unroll
+            for (int v = 0; v < DCV; ++v)
+                raw[v] = __ldg(reinterpret_cast<const uint4*>(row + (int64_t)c * CH + (v * 32 + lane) * VEC));
+        }
+        for (; c < nfull; c += DNW) {
+            float wm, ls;
+            float x[DCV][VEC];
+#pragma unroll
+            for (int v = 0; v < DCV; ++v) unpack_clamped<Tin>(raw[v], x[v]);
+            if (c + DNW < nfull) {
+#pragma unroll
+                for (int v = 0; v < DCV; ++v)
+                    raw[v] = __ldg(reinterpret_cast<const uint4*>(row + (int64_t)(c + DNW) * CH + (v * 32 + lane) * VEC));
+            }
+            chunk_stats<Tin, DCV, GREEDY>(x, (int64_t)c * CH + lane * VEC, bestv, besti, wm, ls);
+            lsum[c * 32 + lane] = ls;
+            if (lane == 0) cmax[c] = wm;
+        }
     }
     if (nfull < nch && warp == (nfull % DNW)) {            // the ragged last chunk
         const int cl = nfull;
@@ -137,14 +231,18 @@ __global__ void __launch_bounds__(DT, 4) draft_kernel(DraftParams p) {
                 for (int q = 0; q < VEC; ++q) x[v][q] = NEG_CLAMP;
             }
         }
-        float wm;
-        double ws;
-        chunk_stats<Tin, DCV, GREEDY>(x, (int64_t)cl * CH + lane * VEC, bestv, besti, wm, ws);
-        if (lane == 0) { cmax[cl] = wm; csum[cl] = ws; }
+        float wm, ls;
+        chunk_stats<Tin, DCV, GREEDY>(x, (int64_t)cl * CH + lane * VEC, bestv, besti, wm, ls);
+        lsum[cl * 32 + lane] = ls;
+        if (lane == 0) cmax[cl] = wm;
     }
     __syncthreads();
 
     // ---- row combine (float64, fixed order): M, Z; non-finite rows -> token -1
+    for (int c = warp; c < nch; c += DNW) {              // chunk sums: fixed-order fp64 warp sums
+        const double ws = warp_sum_d((double)lsum[c * 32 + lane]);
+        if (lane == 0) csum[c] = ws;
+    }
     float m = -INFINITY;
     for (int c = tid; c < nch; c += DT) m = max_nan_f32(m, cmax[c]);
     m = warp_max_nan(m);
@@ -155,7 +253,7 @@ __global__ void __launch_bounds__(DT, 4) draft_kernel(DraftParams p) {
         for (int w = 1; w < DNW; ++w) M = max_nan_f32(M, fred[w]);
         s_M = M;
     }
-    __syncthreads();
+    __syncthreads();                                     // (also orders the csum writes)
     const float M = s_M;
     // chunk weights relative to M, in place (csum[c] <- csum[c] exp(cmax[c] - M))
     double zt = 0.0;
@@ -320,26 +418,28 @@ __global__ void __launch_bounds__(DT, 4) draft_kernel(DraftParams p) {
     }
 }
 
-size_t draft_smem(int64_t V, int bf16) {
+size_t draft_smem(int64_t V, int bf16, int cv) {
     const int VEC = bf16 ? 8 : 4;
-    const int64_t nch = ceil_div(V, 32 * DCV * VEC);
-    return align_up((size_t)nch * 4, 16) + (size_t)nch * 8;
+    const int64_t nch = ceil_div(V, 32 * cv * VEC);
+    return align_up((size_t)nch * 4, 16) + (size_t)nch * 8 + (size_t)nch * 32 * 4;
 }
 
+// chunks of 4 vectors per lane, 4 CTAs per SM (all rows of a 512-request batch resident),
+// 2 of every 8 exponentials on the FMA pipe -- the best of the measured variants
 template <typename Tin, bool G>
-static cudaError_t launch_draft_t(const DraftParams& p, size_t smem, cudaStream_t s) {
+static cudaError_t launch_draft_t(const DraftParams& p, cudaStream_t s) {
+    constexpr int CV = 4, MINB = 4, NPOLY = 2;
+    const size_t smem = draft_smem(p.V, sizeof(Tin) == 2, CV);
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(draft_kernel<Tin, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    draft_kernel<Tin, G><<<p.B, DT, smem, s>>>(p);
+        cudaFuncSetAttribute(draft_kernel<Tin, G, CV, MINB, NPOLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    draft_kernel<Tin, G, CV, MINB, NPOLY><<<p.B, DT, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_draft(const DraftParams& p, int bf16, cudaStream_t s) {
     if (p.B == 0) return cudaSuccess;
-    const size_t smem = draft_smem(p.V, bf16);
-    if (bf16) return p.greedy ? launch_draft_t<__nv_bfloat16, true>(p, smem, s)
-                              : launch_draft_t<__nv_bfloat16, false>(p, smem, s);
-    return p.greedy ? launch_draft_t<float, true>(p, smem, s) : launch_draft_t<float, false>(p, smem, s);
+    if (bf16) return p.greedy ? launch_draft_t<__nv_bfloat16, true>(p, s) : launch_draft_t<__nv_bfloat16, false>(p, s);
+    return p.greedy ? launch_draft_t<float, true>(p, s) : launch_draft_t<float, false>(p, s);
 }
 
 }  // namespace msd
