@@ -329,6 +329,28 @@ __device__ __forceinline__ float exp2f_fma(float x) {
     return r * __int_as_float((ni + 127) << 23);
 }
 
+// 2^x for a pair of x <= 0 on the FMA pipe with packed f32x2 ops, branch-free: x clamped at
+// -127 (-> exactly 0, like ex2.approx.ftz; a NaN x gives 0, so callers detect NaN elsewhere), n = rint(x) by the 1.5*2^23 magic, degree-6
+// Taylor polynomial of e^(t), t = (x - n) ln 2, |t| <= 0.347 (truncation 1.2e-7 relative).
+__device__ __forceinline__ float2 exp2_pair_fma(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 xm = __fadd2_rn(x, magic);
+    const float2 n = __fadd2_rn(xm, make_float2(-12582912.f, -12582912.f));
+    const float2 ln2 = make_float2(0.69314718056f, 0.69314718056f);
+    const float2 t = __fmul2_rn(__fadd2_rn(x, make_float2(-n.x, -n.y)), ln2);
+    float2 r = make_float2(1.38888889e-3f, 1.38888889e-3f);                  // 1/6!
+    r = __ffma2_rn(r, t, make_float2(8.33333333e-3f, 8.33333333e-3f));
+    r = __ffma2_rn(r, t, make_float2(4.16666667e-2f, 4.16666667e-2f));
+    r = __ffma2_rn(r, t, make_float2(1.66666667e-1f, 1.66666667e-1f));
+    r = __ffma2_rn(r, t, make_float2(0.5f, 0.5f));
+    r = __ffma2_rn(r, t, make_float2(1.0f, 1.0f));
+    r = __ffma2_rn(r, t, make_float2(1.0f, 1.0f));
+    const int nx = __float_as_int(xm.x) - 0x4B400000, ny = __float_as_int(xm.y) - 0x4B400000;
+    return __fmul2_rn(r, make_float2(__int_as_float((nx + 127) << 23), __int_as_float((ny + 127) << 23)));
+}
+
 // Combine C slice partials of one row into its RowStat (fixed order -> every CTA
 // that does it gets bit-identical results).  Executed by one full warp.  If `prev`
 // (the previous level's partials of the same slices) is given, the slice KL numerators

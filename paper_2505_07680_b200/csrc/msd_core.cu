@@ -185,6 +185,11 @@ __device__ __forceinline__ float exp2f_fma_any(float x) {
     return exp2f_fma(x);
 }
 
+#ifndef MSD_CORE_NPOLY
+#define MSD_CORE_NPOLY 0
+#endif
+constexpr int CORE_NPOLY = MSD_CORE_NPOLY;   // of every 4 exponential pairs, this many on the FMA pipe
+
 __host__ __device__ constexpr int core_tslots(int L) { return TCOLS / (CET * L); }
 
 // element index (within the slice) of vector jv of pass-1 thread (warp w, lane)
@@ -258,8 +263,14 @@ __device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, f
             yy = __fadd2_rn(xv, nm2);
         }
         const float2 t = __fmul2_rn(yy, l2e);
-        e[2 * pp] = ex2f(t.x);
-        e[2 * pp + 1] = ex2f(t.y);
+        if ((pp & 3) >= 4 - CORE_NPOLY) {              // this pair on the FMA pipe (MUFU relief)
+            const float2 ee = exp2_pair_fma(t);
+            e[2 * pp] = ee.x;
+            e[2 * pp + 1] = ee.y;
+        } else {
+            e[2 * pp] = ex2f(t.x);
+            e[2 * pp + 1] = ex2f(t.y);
+        }
         y[pp] = yy;
     }
 }
@@ -293,8 +304,14 @@ __device__ __forceinline__ void half_exp(const Tin* row, int rg, int lane, int h
             yy = __fadd2_rn(xv, nm2);
         }
         const float2 t = __fmul2_rn(yy, l2e);
-        e[2 * pp] = ex2f(t.x);
-        e[2 * pp + 1] = ex2f(t.y);
+        if ((pp & 3) >= 4 - CORE_NPOLY) {              // this pair on the FMA pipe (MUFU relief)
+            const float2 ee = exp2_pair_fma(t);
+            e[2 * pp] = ee.x;
+            e[2 * pp + 1] = ee.y;
+        } else {
+            e[2 * pp] = ex2f(t.x);
+            e[2 * pp + 1] = ex2f(t.y);
+        }
         y[pp] = yy;
     }
 }

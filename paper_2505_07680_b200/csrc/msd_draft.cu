@@ -84,28 +84,6 @@ __device__ __forceinline__ void chunk_stats(const float (&x)[CV][Elem<Tin>::VEC]
     ls = s;
 }
 
-// 2^x for a pair of x <= 0 on the FMA pipe with packed f32x2 ops, branch-free: x clamped at
-// -127 (-> exactly 0, like ex2.approx.ftz), n = rint(x) by the 1.5*2^23 magic, degree-6
-// Taylor polynomial of e^(t), t = (x - n) ln 2, |t| <= 0.347 (truncation 1.2e-7 relative).
-__device__ __forceinline__ float2 exp2_pair_fma(float2 x) {
-    x.x = fmaxf(x.x, -127.f);
-    x.y = fmaxf(x.y, -127.f);
-    const float2 magic = make_float2(12582912.f, 12582912.f);
-    const float2 xm = __fadd2_rn(x, magic);
-    const float2 n = __fadd2_rn(xm, make_float2(-12582912.f, -12582912.f));
-    const float2 ln2 = make_float2(0.69314718056f, 0.69314718056f);
-    const float2 t = __fmul2_rn(__fadd2_rn(x, make_float2(-n.x, -n.y)), ln2);
-    float2 r = make_float2(1.38888889e-3f, 1.38888889e-3f);                  // 1/6!
-    r = __ffma2_rn(r, t, make_float2(8.33333333e-3f, 8.33333333e-3f));
-    r = __ffma2_rn(r, t, make_float2(4.16666667e-2f, 4.16666667e-2f));
-    r = __ffma2_rn(r, t, make_float2(1.66666667e-1f, 1.66666667e-1f));
-    r = __ffma2_rn(r, t, make_float2(0.5f, 0.5f));
-    r = __ffma2_rn(r, t, make_float2(1.0f, 1.0f));
-    r = __ffma2_rn(r, t, make_float2(1.0f, 1.0f));
-    const int nx = __float_as_int(xm.x) - 0x4B400000, ny = __float_as_int(xm.y) - 0x4B400000;
-    return __fmul2_rn(r, make_float2(__int_as_float((nx + 127) << 23), __int_as_float((ny + 127) << 23)));
-}
-
 // bf16 chunk straight from the loaded words: max.NaN.bf16x2 for the lane maximum, then per
 // pair FHADD.BF16 (x - wm without unpacking), one FMUL2 by log2 e, ex2 (every 8th element on
 // the FMA pipe) and FADD2 partial sums -- about 3.5 issue slots per element.  Same values
