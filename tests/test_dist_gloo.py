@@ -48,6 +48,16 @@ def _pair_stats(inp):
     return st
 
 
+def _pool_stats(inp):
+    """[L(L-1)/2, 8] int64 bootstrap stats of a shard's draft rows, via the oracle."""
+    dtv, _ = oracle.pool_divergence([t[:, :K].numpy() for t in inp.levels])
+    st = np.zeros((dtv.shape[0], 8), np.int64)
+    for q in range(dtv.shape[0]):
+        st[q, 0] = int(sum(int(np.rint(min(max(x, 0.0), 1.0) * DTV_SCALE)) for x in dtv[q].ravel()))
+        st[q, 2] = dtv[q].size
+    return st
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -65,7 +75,12 @@ def _worker(rank, world, port, q):
         mdist.allreduce_stats(stats)
         sch = mdist.ChainScheduler(T_ms=[1.0, 3.0, 10.0], W=K)
         chain = sch.update(stats.tolist())
-        q.put((r, req0, b, stats.numpy().copy(), chain, sch.t_eff, [t[:, :, :8].clone() for t in inp.levels]))
+        pool = torch.from_numpy(_pool_stats(inp))
+        mdist.allreduce_stats(pool)
+        boot = mdist.ChainScheduler(T_ms=[1.0, 3.0, 10.0], W=K)
+        bchain = boot.bootstrap(pool.tolist())
+        q.put((r, req0, b, stats.numpy().copy(), chain, sch.t_eff, [t[:, :, :8].clone() for t in inp.levels],
+               pool.numpy().copy(), bchain, boot.sim))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # surface the failure in the parent
@@ -102,13 +117,13 @@ def test_shards_are_disjoint_and_cover_the_batch():
 
 def test_sharded_inputs_equal_unsharded(two_ranks):
     full = _inputs(2 * B_LOCAL, 0)
-    for r, req0, b, _, _, _, lv in two_ranks:
+    for r, req0, b, _, _, _, lv in (o[:7] for o in two_ranks):
         for l in range(L):
             assert torch.equal(lv[l], full.levels[l][req0:req0 + b, :, :8])
 
 
 def test_allreduced_stats_identical_and_exact(two_ranks):
-    (_, _, _, s0, c0, t0, _), (_, _, _, s1, c1, t1, _) = two_ranks
+    (_, _, _, s0, c0, t0), (_, _, _, s1, c1, t1) = (o[:6] for o in two_ranks)
     assert np.array_equal(s0, s1)
     single = _pair_stats(_inputs(2 * B_LOCAL, 0))
     assert np.array_equal(s0, single)          # integer sums: G-invariant, bit-exact
@@ -117,7 +132,7 @@ def test_allreduced_stats_identical_and_exact(two_ranks):
 
 
 def test_scheduler_decision_matches_single_process(two_ranks):
-    _, _, _, s0, c0, t0, _ = two_ranks[0]
+    _, _, _, s0, c0, t0 = two_ranks[0][:6]
     single = _pair_stats(_inputs(2 * B_LOCAL, 0))
     sch = mdist.ChainScheduler(T_ms=[1.0, 3.0, 10.0], W=K)
     assert sch.update(single.tolist()) == c0
@@ -130,3 +145,17 @@ def test_scheduler_decision_matches_single_process(two_ranks):
 def test_allreduce_rejects_non_integer_stats():
     with pytest.raises(TypeError):
         mdist.allreduce_stats(torch.zeros(2, 8))
+
+
+def test_bootstrap_stats_and_decision_match_single_process(two_ranks):
+    """SimScore bootstrap across ranks: the all-reduced pool stats are bit-identical
+    on both ranks and equal to the single-process totals, so both ranks bootstrap the same
+    P x P SimScore matrix and take the same Alg. 1 decision."""
+    p0, b0, m0 = two_ranks[0][7:10]
+    p1, b1, m1 = two_ranks[1][7:10]
+    assert np.array_equal(p0, p1) and b0 == b1 and m0 == m1
+    single = _pool_stats(_inputs(2 * B_LOCAL, 0))
+    assert np.array_equal(p0, single)
+    sch = mdist.ChainScheduler(T_ms=[1.0, 3.0, 10.0], W=K)
+    assert sch.bootstrap(single.tolist()) == b0
+    assert sch.sim == m0
