@@ -216,10 +216,20 @@ __device__ bool slice_partial_bf16(const __nv_bfloat16* row, int64_t s0, int64_t
     return true;
 }
 
+// Every 128-byte line of a row requested into L2 by the whole CTA (no registers held).
+template <typename Tin>
+__device__ __forceinline__ void prefetch_row_l2(const Tin* row, int64_t V) {
+    const char* b0 = reinterpret_cast<const char*>(row);
+    const int64_t nb = V * (int64_t)sizeof(Tin);
+    for (int64_t o = (int64_t)threadIdx.x * 128; o < nb; o += (int64_t)blockDim.x * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b0 + o));
+}
+
 template <typename Tin>
 __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShared& sh, bool want_am = true) {
     constexpr int VEC = Elem<Tin>::VEC;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    prefetch_row_l2(row, V);    // the slices below then stream from L2, not one HBM trip per 4 vectors
     for (int s = warp; s < C; s += NWARP) {
         if (sizeof(Tin) == 2) {
             Partial pr;

@@ -48,3 +48,10 @@ for r in order[:3]:
     print(f"  req {r} phases (cycles): " + "  ".join(f"{n} {rq[r, k]:.0f}" for k, n in enumerate(names)))
 med = np.argsort(dur)[B // 2]
 print(f"  median req {med} phases (cycles): " + "  ".join(f"{n} {rq[med, k]:.0f}" for k, n in enumerate(names)))
+
+# per-phase cycles (thread 0) of the slowest requests
+rq = np.frombuffer(req0, dtype=np.uint64).reshape(4096, 16)[:B].astype(np.float64)
+print("phases of the slowest requests (cycles):", names)
+for r in order[:5]:
+    print(f"  req {r}: " + " ".join(f"{rq[r, k]:.0f}" for k in range(len(names))))
+print("median request:", " ".join(f"{np.median(rq[:, k]):.0f}" for k in range(len(names))))
