@@ -391,6 +391,16 @@ struct ExpShift {
     }
 };
 
+// Table path of ExpShift for a batch of N values: every gather issued before any is used (the
+// exact draw is bound by table-gather latency otherwise); same value as ExpShift::operator().
+template <int N>
+__device__ __forceinline__ void exp_shift_batch(const ExpShift& es, const float* z, double* out) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = __ldg(es.tab + (__float_as_uint(z[k]) >> 16));
+#pragma unroll
+    for (int k = 0; k < N; ++k) out[k] = (out[k] == out[k]) ? out[k] * es.eS : dexp_neg((double)z[k] - es.S);
+}
+
 __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, double B) {
     if (!(za > NEG_MASKED)) return 0.0;
     const double pa = dexp_neg((double)za - A);     // z <= max <= lse: argument <= 0
@@ -574,7 +584,7 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
 // Exact float64 draw over the whole row (pair): exact normalisers, exact slice masses (one
 // warp per slice, fixed order), exact scan.  Residual mass < 1e-12 -> draw from p.
 template <typename Tin>
-__device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const RowStat& Ar,
+__device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const RowStat& Ar,
                               const RowStat& Br, int64_t V, int C, int vse, double u, TailShared& sh,
                               bool* tie, bool* small) {
   constexpr int VEC = Elem<Tin>::VEC;
@@ -582,6 +592,10 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
 #ifdef MSD_PROF
   if (threadIdx.x == 0) g_tail_req[blockIdx.x][11] += (unsigned long long)clock64();
 #endif
+  // both rows into L2 up front: the normaliser pass then has every line in flight, and the
+  // slice-mass pass and the rescan below re-read them from L2
+  prefetch_row_l2(ra, V);
+  if (resid) prefetch_row_l2(rb, V);
   // exact normalisers: every thread a strided set of whole vectors, 4 in flight
   const double* tab = sizeof(Tin) == 2 ? sh.exptab : nullptr;
   ExpShift eMa, eMb;
@@ -597,12 +611,26 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
               load_vec<Tin>(ra, e0 + (int64_t)uu * T * VEC, V, xa[uu]);
               if (resid) load_vec<Tin>(rb, e0 + (int64_t)uu * T * VEC, V, xb[uu]);
           }
+          if (eMa.tab && (!resid || eMb.tab)) {
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu) {
+              for (int uu = 0; uu < U; ++uu) {
+                  double ga[VEC], gb[VEC];
+                  exp_shift_batch<VEC>(eMa, xa[uu], ga);
+                  if (resid) exp_shift_batch<VEC>(eMb, xb[uu], gb);
 #pragma unroll
-              for (int k = 0; k < VEC; ++k) {
-                  if (xa[uu][k] > NEG_MASKED) sa += eMa(xa[uu][k]);
-                  if (resid && xb[uu][k] > NEG_MASKED) sb += eMb(xb[uu][k]);
+                  for (int k = 0; k < VEC; ++k) {
+                      if (xa[uu][k] > NEG_MASKED) sa += ga[k];
+                      if (resid && xb[uu][k] > NEG_MASKED) sb += gb[k];
+                  }
+              }
+          } else {
+#pragma unroll
+              for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+                  for (int k = 0; k < VEC; ++k) {
+                      if (xa[uu][k] > NEG_MASKED) sa += eMa(xa[uu][k]);
+                      if (resid && xb[uu][k] > NEG_MASKED) sb += eMb(xb[uu][k]);
+                  }
               }
           }
       }
@@ -631,10 +659,31 @@ __device__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const Ro
                 load_vec<Tin>(ra, e0 + (int64_t)uu * 32 * VEC, s1, xa[uu]);
                 if (resid) load_vec<Tin>(rb, e0 + (int64_t)uu * 32 * VEC, s1, xb[uu]);
             }
+            if (eA.tab && (!resid || eB.tab)) {
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu) {
+                for (int uu = 0; uu < U; ++uu) {
+                    double ga[VEC], gb[VEC];
+                    exp_shift_batch<VEC>(eA, xa[uu], ga);
+                    if (resid) exp_shift_batch<VEC>(eB, xb[uu], gb);
 #pragma unroll
-                for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[uu][k], resid ? xb[uu][k] : NEG_CLAMP, eA, eB);
+                    for (int k = 0; k < VEC; ++k) {    // = wt(resid, za, zb, eA, eB)
+                        double w = 0.0;
+                        if (xa[uu][k] > NEG_MASKED) {
+                            w = ga[k];
+                            if (resid) {
+                                const double r = w - ((xb[uu][k] > NEG_MASKED) ? gb[k] : 0.0);
+                                w = r > 0.0 ? r : 0.0;
+                            }
+                        }
+                        acc += w;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[uu][k], resid ? xb[uu][k] : NEG_CLAMP, eA, eB);
+                }
             }
         }
         acc = warp_sum_d(acc);

@@ -55,3 +55,6 @@ print("phases of the slowest requests (cycles):", names)
 for r in order[:5]:
     print(f"  req {r}: " + " ".join(f"{rq[r, k]:.0f}" for k in range(len(names))))
 print("median request:", " ".join(f"{np.median(rq[:, k]):.0f}" for k in range(len(names))))
+ex = [r for r in range(B) if int(fl[r]) & api.FLAG['EXACT_DRAW']]
+for r in ex[:4]:
+    print(f"  exact-draw req {r}: normalisers {rq[r, 9] - rq[r, 11]:.0f} cycles, slice masses {rq[r, 10] - rq[r, 9]:.0f} cycles")
