@@ -113,3 +113,27 @@ def test_empty_batch_and_argument_errors():
         api.draft_sample(y, u, row=2)
     with pytest.raises(RuntimeError):
         api.draft_sample(y, None)                          # stochastic mode needs u
+
+
+def test_extreme_logits_and_uniform_endpoints():
+    """Peaked rows (one logit 1e4 above the rest: every other weight underflows), flat rows
+    (all equal: token = floor(u V)), u = 0 and the largest float below 1."""
+    V = 50000
+    z = torch.zeros((6, 1, V), dtype=torch.float32, device=DEV)
+    z[0, 0, 123] = 1e4
+    z[1, 0, :] = -3.0                                       # flat
+    z[2, 0, :] = -3.0
+    z[3, 0, :] = torch.linspace(-40, 40, V, device=DEV)     # monotone
+    z[4, 0, ::2] = float("-inf")                            # every other token masked, rest flat
+    z[5, 0, :] = 7.0
+    one_minus = float(np.nextafter(np.float32(1), np.float32(0)))
+    u = torch.tensor([0.7, 0.0, one_minus, 0.5, 0.3, 0.25], dtype=torch.float32, device=DEV)
+    out = api.draft_sample(z, u)
+    torch.cuda.synchronize()
+    ref = oracle.draft_sample(z[:, 0].double().cpu().numpy(), u.cpu().numpy(), tie_eps_draw=DRAW_BAND)
+    tok = out["token"].cpu().numpy()
+    assert tok[0] == 123 and tok[1] == 0 and tok[2] == V - 1
+    ok = ref["near_tie"] == 0
+    assert np.array_equal(tok[ok], ref["token"][ok])
+    assert tok[4] % 2 == 1
+    assert np.allclose(out["lse"].double().cpu().numpy(), ref["lse"], rtol=1e-6, atol=1e-5)
