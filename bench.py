@@ -323,7 +323,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "positions/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": c["dtype"], "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": args.config, "global_batch": B * ws if args.scaling == "weak" else cfg["B"],
                        "batch_per_gpu": B, "V": V, "K": K, "L": L, "logits": c["dtype"],
                        "sigmas": list(c["sigmas"]), "parallelism": f"dp{ws} (requests sharded)",
