@@ -707,6 +707,40 @@ __device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin*
   return 0;
 }
 
+// Block-wide copy of `bytes` (a multiple of 8) from global to shared memory with every load of
+// a thread issued before its stores (one memory round trip instead of one per word): 16-byte
+// words when both sides allow it, else 8-byte words.
+__device__ __forceinline__ void copy_to_smem(void* dst, const void* src, size_t bytes) {
+    constexpr int U = 8;
+    if ((((uintptr_t)dst | (uintptr_t)src | bytes) & 15) == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        const size_t n = bytes / 16;
+        for (size_t t0 = threadIdx.x; t0 < n; t0 += (size_t)U * T) {
+            uint4 v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (t0 + (size_t)k * T < n) v[k] = s4[t0 + (size_t)k * T];
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (t0 + (size_t)k * T < n) d4[t0 + (size_t)k * T] = v[k];
+        }
+    } else {
+        const unsigned long long* s8 = reinterpret_cast<const unsigned long long*>(src);
+        unsigned long long* d8 = reinterpret_cast<unsigned long long*>(dst);
+        const size_t n = bytes / 8;
+        for (size_t t0 = threadIdx.x; t0 < n; t0 += (size_t)U * T) {
+            unsigned long long v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (t0 + (size_t)k * T < n) v[k] = s8[t0 + (size_t)k * T];
+#pragma unroll
+            for (int k = 0; k < U; ++k)
+                if (t0 + (size_t)k * T < n) d8[t0 + (size_t)k * T] = v[k];
+        }
+    }
+}
+
 template <typename Tin>
 #ifndef MSD_TAIL_MINB
 #define MSD_TAIL_MINB 2
@@ -738,12 +772,9 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
     const Partial* part_b = p.partials + (size_t)b * npart;
     const double* res_b = p.resid + (size_t)b * nres;
     if (pre) {
-        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(part_b);
-        unsigned long long* dst = reinterpret_cast<unsigned long long*>(tdyn);
-        const size_t nw = npart * sizeof(Partial) / 8;
-        for (size_t t = tid; t < nw; t += T) dst[t] = src[t];
         double* rd = reinterpret_cast<double*>(tdyn + npart * sizeof(Partial));
-        for (size_t t = tid; t < nres; t += T) rd[t] = res_b[t];
+        copy_to_smem(tdyn, part_b, npart * sizeof(Partial));
+        copy_to_smem(rd, res_b, nres * sizeof(double));
         part_b = reinterpret_cast<const Partial*>(tdyn);
         res_b = rd;
     }
