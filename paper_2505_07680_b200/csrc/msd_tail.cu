@@ -784,6 +784,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
         sh.zpre[l][i] = (x >= 0 && x < V) ? clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l, b, i) + x)) : NEG_CLAMP;
     }
     __syncthreads();
+    TPROF(12)
     // row normalisers (Eq. 1) and KL numerators of every draft-position row, combined from
     // the core's slice partials in a fixed order (one warp per row)
     for (int r = warp; r < K * L; r += NWARP) {
@@ -794,6 +795,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
         if (lane == 0) { sh.row[i][l] = rs; sh.kl[i][l] = Kl; }
     }
     __syncthreads();
+    TPROF(13)
     if (tid < K) {
         const int i = tid;
         bool bad = false;

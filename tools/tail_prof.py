@@ -58,3 +58,4 @@ print("median request:", " ".join(f"{np.median(rq[:, k]):.0f}" for k in range(le
 ex = [r for r in range(B) if int(fl[r]) & api.FLAG['EXACT_DRAW']]
 for r in ex[:4]:
     print(f"  exact-draw req {r}: normalisers {rq[r, 9] - rq[r, 11]:.0f} cycles, slice masses {rq[r, 10] - rq[r, 9]:.0f} cycles")
+print("prologue split (median cycles): prefetch+gathers", f"{np.median(rq[:, 12]):.0f}", " row combines", f"{np.median(rq[:, 13]):.0f}", " rest of 'combine rows'", f"{np.median(rq[:, 0]):.0f}")
