@@ -395,24 +395,31 @@ double or_ema(double old_value, double measured, double weight, int32_t first) {
 }
 
 /* Eq. 7 with the continuous acceptance composition of S:457:
- * L_1 = W; fed_j = W for j = 2, else L_{j-1} (+1 with intermediate bonus);
- * L_j = alpha_j (1 - alpha_j^{fed_j}) / (1 - alpha_j)  (= fed_j at alpha_j = 1);
- * tokens per cycle = L_N + 1; latency = W T_1 + sum_{j>=2} cost_j with
- * cost_j = T_j (one verify pass, Eq. 4 convention) or W T_j ("W x T_j").
- * Chain [M_t] alone: T_eff = T_t. */
+ * L_1 = W (the drafter proposes W tokens) and fed_2 = W;
+ * L_j = alpha_j (1 - alpha_j^{fed_j}) / (1 - alpha_j)  (= fed_j at alpha_j = 1), the expected
+ *       number of the fed_j candidates that level j accepts (a run of Bernoulli(alpha_j) tests
+ *       that stops at the first rejection);
+ * fed_{j+1} = L_j + 1 with the intermediate bonus: level j always emits one token, the
+ *       correction on a rejection or the bonus after a full acceptance;
+ * fed_{j+1} = L_j + (1 - alpha_j^{fed_j}) without it: the correction token is still emitted on
+ *       a rejection, whose probability is 1 - alpha_j^{fed_j} (continuous extension);
+ * tokens per cycle = L_N + 1 (the target's correction or bonus); latency = W T_1 +
+ * sum_{j>=2} cost_j with cost_j = T_j (one verify pass, Eq. 4 convention) or W T_j (P:189
+ * "W x T_j").  Chain [M_t] alone: T_eff = T_t. */
 double or_predict_chain_latency(int32_t N, const double* T, const double* alpha, int32_t W,
                                 int32_t verify_linear, int32_t intermediate_bonus) {
     if (N <= 1) return T[0];
-    double Lprev = (double)W;
+    double fed = (double)W;
+    double Lj = 0.0;
     double latency = (double)W * T[0];
     for (int32_t j = 1; j < N; ++j) {
-        double fed = (j == 1) ? (double)W : Lprev + (intermediate_bonus ? 1.0 : 0.0);
         double a = alpha[j - 1];
-        double Lj = (a >= 1.0) ? fed : a * (1.0 - pow(a, fed)) / (1.0 - a);
+        double p_all = (a >= 1.0) ? 1.0 : pow(a, fed);       /* all fed candidates accepted */
+        Lj = (a >= 1.0) ? fed : a * (1.0 - p_all) / (1.0 - a);
         latency += verify_linear ? (double)W * T[j] : T[j];
-        Lprev = Lj;
+        fed = Lj + (intermediate_bonus ? 1.0 : (1.0 - p_all));
     }
-    return latency / (Lprev + 1.0);
+    return latency / (Lj + 1.0);
 }
 
 /* Alg. 1 by exhaustive enumeration: every strictly increasing

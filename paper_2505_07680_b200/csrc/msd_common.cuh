@@ -352,12 +352,10 @@ __device__ __forceinline__ float2 exp2_pair_fma(float2 x) {
 }
 
 // Combine C slice partials of one row into its RowStat (fixed order -> every CTA
-// that does it gets bit-identical results).  Executed by one full warp.  If `prev`
-// (the previous level's partials of the same slices) is given, the slice KL numerators
-// are stored relative to the slice shift m_s - m'_s and that shift is restored here in
-// float64: K = sum_s (K_s + (m_s - m'_s) S_s) e^{m_s - M}.
-__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out,
-                                      const Partial* prev = nullptr) {
+// that does it gets bit-identical results).  Executed by one full warp.  The slice KL
+// numerators K_s = sum_{v in s} e^{z_v - m_s} (z_v - z'_v) (raw logit differences) are
+// rescaled to the row maximum in float64: K = sum_s K_s e^{m_s - M}.
+__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out) {
     const int lane = threadIdx.x & 31;
     float m = -INFINITY;
     for (int s = lane; s < C; s += 32) m = fmaxf(m, parts[s].m);
@@ -368,11 +366,9 @@ __device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out
     for (int s = lane; s < C; s += 32) {
         float ms = parts[s].m;
         double Ss = parts[s].S;
-        double Ks = parts[s].Kl;
         double f = dexp_neg((double)ms - (double)m);
         S += Ss * f;
-        if (prev) Ks += ((double)ms - (double)prev[s].m) * Ss;
-        Kl += Ks * f;
+        Kl += parts[s].Kl * f;
         if (ms == m) am = min(am, parts[s].amax);
         if (isnan(ms) || isnan(Ss)) bad = true;
     }

@@ -60,6 +60,9 @@ constexpr int TCOLS = 256;             // TMEM columns per region (2 regions per
 #define MSD_NFETCH 2
 #endif
 constexpr int NFETCH = MSD_NFETCH;
+#ifndef MSD_LDGSTS
+#define MSD_LDGSTS 0                   // 1: the producer streams with 16-byte cp.async instead of bulk copies
+#endif
 // Warp numbering: latency-critical service warps first, then pass 2, then the throughput
 // warps (pass 1).  Pass-1 warp W_P1 + r owns region r in TMEM lane quadrant r % 4; pass-2
 // warp W_P2 + v serves regions v and v + 4 (quadrant v): both bases are multiples of 4.
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     if (warp == W_PROD) {
         if (lane == 0) {
             // empty: one arrival per region (pass-1 warps for T items, pass-2 warps for R items)
-            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], nact); }
+            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], MSD_LDGSTS ? 32 : 1); mbar_init(&c.empty[s], nact); }
             for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], nact); mbar_init(&c.r1_empty[r], 1); }
             for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], np2); mbar_init(&c.r2_empty[r], 1); }
             for (int k = 0; k < NQ; ++k) {
@@ -473,6 +476,12 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int r1 = j & (R1 - 1);
                 Tin* stage = ring + (size_t)cu.st * L * RS;
                 mbar_wait(&c.full[cu.st], (uint32_t)cu.sph);
+                if (p.dbg & 4) {   // debug: the TMA ring alone (no pass-1 arithmetic)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&c.empty[cu.st]);
+                    for (int x = 0; x < NG1; ++x) cu.next(S, PP, PT, NT);
+                    continue;
+                }
                 PROF(0)
                 if (rg == 0 && lane == 0) stamp(j, 1);
                 // a row length that is not a multiple of 16 bytes: patch the straddling vector
@@ -528,11 +537,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                             const float2 e23 = __fadd2_rn(make_float2(e[4], e[5]), make_float2(e[6], e[7]));
                             s2[l] = __fadd2_rn(s2[l], __fadd2_rn(e01, e23));
                             if (l > 0) {
+                                // KL numerator sum e_l (z_l - z_{l-1}): the raw logit difference
+                                // (y_l - y_{l-1}) + (m_l - m_{l-1}) is exact in fp32, so the
+                                // O(1) cancellation against the normaliser difference happens
+                                // later in fp64 (R18)
                                 const float2 neg1 = make_float2(-1.f, -1.f);
-                                float2 ka = __fmul2_rn(make_float2(e[0], e[1]), __ffma2_rn(yprev[0], neg1, y[0]));
-                                float2 kb = __fmul2_rn(make_float2(e[2], e[3]), __ffma2_rn(yprev[1], neg1, y[1]));
-                                ka = __ffma2_rn(make_float2(e[4], e[5]), __ffma2_rn(yprev[2], neg1, y[2]), ka);
-                                kb = __ffma2_rn(make_float2(e[6], e[7]), __ffma2_rn(yprev[3], neg1, y[3]), kb);
+                                const float2 cm = make_float2(wm[l] - wm[l - 1], wm[l] - wm[l - 1]);
+                                float2 ka = __fmul2_rn(make_float2(e[0], e[1]), __fadd2_rn(__ffma2_rn(yprev[0], neg1, y[0]), cm));
+                                float2 kb = __fmul2_rn(make_float2(e[2], e[3]), __fadd2_rn(__ffma2_rn(yprev[1], neg1, y[1]), cm));
+                                ka = __ffma2_rn(make_float2(e[4], e[5]), __fadd2_rn(__ffma2_rn(yprev[2], neg1, y[2]), cm), ka);
+                                kb = __ffma2_rn(make_float2(e[6], e[7]), __fadd2_rn(__ffma2_rn(yprev[3], neg1, y[3]), cm), kb);
                                 k2[l] = __fadd2_rn(k2[l], __fadd2_rn(ka, kb));
                             }
 #pragma unroll
@@ -770,7 +784,36 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     } else if (warp == W_PROD) {
         // ================================================================ TMA producer
         PROF_DECL
+#if MSD_LDGSTS
+        // the whole warp issues 16-byte cp.async (LDGSTS) copies; each lane's copies complete
+        // on the stage's full barrier (count 32, arrive.noinc)
+        {
+            const uint64_t pol = policy_evict_first();
+            const int nvec = len_bulk * ES / 16;
+            Cursor cu;
+            for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
+                const int j = cu.j;
+                if (j >= S) mbar_wait(&c.empty[cu.st], (uint32_t)(cu.sph ^ 1));
+                int64_t u, b, i;
+                item(j, u, b, i);
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    const uint32_t dst = smem_u32(ring + ((size_t)cu.st * L + l) * RS);
+                    const char* src = reinterpret_cast<const char*>(reinterpret_cast<const Tin*>(p.lv.ptr[l]) +
+                                                                    b * p.lv.bs[l] + i * p.lv.ld[l] + base);
+                    for (int x = lane; x < nvec; x += 32)
+                        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst + 16 * x),
+                                     "l"(src + 16 * (size_t)x), "l"(pol)
+                                     : "memory");
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&c.full[cu.st]))
+                             : "memory");
+            }
+        }
+        if (false) {
+#else
         if (lane == 0) {
+#endif
             const uint64_t pol = policy_evict_first();
             const uint32_t bytes = (uint32_t)(len_bulk * ES);   // [len_bulk, RS) holds the pad
             Cursor cu;
@@ -814,7 +857,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int r1 = j & (R1 - 1);
             mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
             PROF(0)
-            float Sw = 0.f, Kw = 0.f, wm = -INFINITY, wmp = -INFINITY;
+            float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
             int aw = 0x7fffffff;
             if (act) {
                 const float4 s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
@@ -822,7 +865,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 Sw = (s4.x + s4.y) + (s4.z + s4.w);
                 Kw = (k4.x + k4.y) + (k4.z + k4.w);
                 wm = c.wmx[k][l][w];
-                wmp = c.wmx[k][l > 0 ? l - 1 : 0][w];
                 if (GREEDY) aw = c.r1A[r1][l][w];
             }
             __syncwarp();
@@ -832,15 +874,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             float msl = wm;
 #pragma unroll
             for (int o = 4; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
-            const float mslp = __shfl_sync(0xffffffffu, msl, (lane - 8) & 31);   // previous row's
             float f = wm == msl ? 1.f : ex2f((wm - msl) * LOG2E);
             if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
-            float Sx = Sw * f, Kx = 0.f;
-            if (l > 0 && f != 0.f) {
-                // KL numerator relative to the slice shift sigma = m_s,l - m_s,l-1
-                const float dsh = (wm - wmp) - (msl - mslp);
-                Kx = f * fmaf(dsh, Sw, Kw);
-            }
+            // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
+            float Sx = Sw * f, Kx = (l > 0 && f != 0.f) ? f * Kw : 0.f;
             int ax = (wm == msl) ? aw : 0x7fffffff;
             PROF(3)
 #pragma unroll

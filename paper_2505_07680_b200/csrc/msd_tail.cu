@@ -791,7 +791,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
         const int i = r / L, l = r % L;
         double Kl;
         const Partial* pp = part_b + ((size_t)i * L + l) * C;
-        RowStat rs = combine_row(pp, C, &Kl, l > 0 ? pp - C : nullptr);
+        RowStat rs = combine_row(pp, C, &Kl);   // slice KL numerators are raw: sum e (z_l - z_{l-1})
         if (lane == 0) { sh.row[i][l] = rs; sh.kl[i][l] = Kl; }
     }
     __syncthreads();

@@ -5,7 +5,7 @@ import torch
 import oracle
 
 DIV_REL, DIV_ABS = 1e-4, 1e-7     # DESIGN.md R18
-KL_ABS = 5e-7                     # DESIGN.md R18: fp32 KL numerator, 2^-21 absolute
+KL_ABS = 1e-7                     # DESIGN.md R18
 ACCEPT_BAND = 1e-6                # north star: |u - p/q| < 1e-6
 DRAW_BAND = 1e-7                  # inverse-CDF draws: |u - C/Z| < 1e-7 (tighter than R18's 1e-6)
 

@@ -52,25 +52,73 @@ def test_host_cost_model_spec_examples():
         api.predict_chain_latency([1.0, 2.0], [1.5], 4)                          # alpha > 1
 
 
-def test_host_cost_model_matches_oracle_eq7_and_alg1():
+def _run_mean(a, fed):
+    """E[accepted run] of fed candidates with Bernoulli(a) tests stopping at the first
+    rejection, summed over its law (P(acc = i) = a^i (1 - a), i < fed; P(acc = fed) = a^fed)."""
+    return sum(i * a ** i * (1 - a) for i in range(fed)) + fed * a ** fed
+
+
+def test_host_eq7_two_level_equals_eq4_and_deterministic_three_level():
+    # pinned by the paper, not by the oracle: N = 2 with one verify pass is Eq. 4's speedup
+    # (P:82, S:487), and alpha_2 in {0, 1} makes a 3-level cycle deterministic up to the
+    # target's run, whose mean is summed from its law
     import numpy as np
-    import oracle
     rng = np.random.default_rng(0)
-    for _ in range(200):
-        N = int(rng.integers(1, 5))
-        T = list(rng.random(N) * 10 + 0.1)
-        a = list(rng.random(N - 1))
-        W = int(rng.integers(1, 9))
-        for vc in (0, 1):
-            for ib in (0, 1):
-                assert api.predict_chain_latency(T, a, W, vc, ib) == pytest.approx(
-                    oracle.predict_chain_latency(T, a, W, vc, ib), rel=1e-12)
-    for _ in range(100):
+    for _ in range(50):
+        a, g, c = rng.random(), int(rng.integers(1, 12)), rng.random() * 0.5 + 0.01
+        Tp = 40.0
+        te = api.predict_chain_latency([c * Tp, Tp], [a], g)
+        assert Tp / te == pytest.approx((1 - a ** (g + 1)) / ((1 - a) * (g * c + 1)), rel=1e-12)
+    T = [1.0, 5.0, 40.0]
+    for ib in (0, 1):
+        for W in (1, 3, 7):
+            for a3 in (0.2, 0.5, 0.9):
+                lat = W * T[0] + T[1] + T[2]
+                assert api.predict_chain_latency(T, [0.0, a3], W, 0, ib) == pytest.approx(
+                    lat / (1 + _run_mean(a3, 1)), rel=1e-12)
+                assert api.predict_chain_latency(T, [1.0, a3], W, 0, ib) == pytest.approx(
+                    lat / (1 + _run_mean(a3, W + ib)), rel=1e-12)
+
+
+@pytest.mark.parametrize("ibonus", [0, 1])
+@pytest.mark.parametrize("linear", [0, 1])
+def test_host_eq7_three_level_monte_carlo(ibonus, linear):
+    # SPEC.md:462: predicted T_eff within 10% of the simulated cascade over 10^4 cycles
+    import itertools
+    from tests._costmc import simulate_t_eff
+    T = [1.0, 5.0, 40.0]
+    for a2, a3 in itertools.product((0.3, 0.6, 0.85, 0.97), repeat=2):
+        for W in (2, 4, 8):
+            pred = api.predict_chain_latency(T, [a2, a3], W, linear, ibonus)
+            mc = simulate_t_eff(T, [a2, a3], W, bool(linear), bool(ibonus), cycles=10_000, seed=W)
+            assert pred == pytest.approx(mc, rel=0.10), (a2, a3, W)
+
+
+def test_host_select_chain_is_the_brute_force_argmin():
+    # SPEC.md:470-471: selection = exhaustive argmin of the predicted T_eff over every
+    # capability-ordered chain ending at the target (length <= max_len), ties -> shorter, then
+    # lexicographic ids; the candidates are enumerated here with itertools
+    import itertools
+    import numpy as np
+    rng = np.random.default_rng(1)
+    for trial in range(150):
         P = int(rng.integers(1, 6))
-        T = np.sort(rng.random(P) * 10 + 0.1)
+        T = list(np.sort(rng.random(P) * 10 + 0.1))
         sim = rng.random((P, P))
+        if trial % 3 == 0:
+            sim = np.round(sim, 1)          # exact ties between chains
         W = int(rng.integers(1, 9))
-        assert api.select_chain(T, sim, W, 4)[0] == oracle.select_chain(T, sim, W, 4)[0]
+        max_len = int(rng.integers(1, 5))
+        for vc, ib in ((0, 1), (1, 0)):
+            cands = []
+            for n in range(0, min(P - 1, max_len - 1) + 1):
+                for pre in itertools.combinations(range(P - 1), n):
+                    ch = list(pre) + [P - 1]
+                    a = [min(1.0, max(0.0, sim[ch[j]][ch[j + 1]])) for j in range(len(ch) - 1)]
+                    cands.append((api.predict_chain_latency([T[m] for m in ch], a, W, vc, ib), len(ch), ch))
+            best = min(cands)
+            ch, te = api.select_chain(T, sim, W, max_len, vc, ib)
+            assert ch == best[2] and te == best[0]
 
 
 def test_simscore_update_ema():

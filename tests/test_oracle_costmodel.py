@@ -81,3 +81,56 @@ def test_select_chain_respects_max_len():
     sim = np.full((4, 4), 0.95)
     ch, _ = O.select_chain(T, sim, 8, max_len=2)
     assert len(ch) <= 2 and ch[-1] == 3
+
+
+# ------------------------------------------------------------------ Eq. 7 for N >= 3
+import itertools
+
+from tests._costmc import simulate_t_eff
+
+
+@pytest.mark.parametrize("ibonus", [True, False])
+@pytest.mark.parametrize("linear", [False, True])
+def test_eq7_three_level_monte_carlo(ibonus, linear):
+    # [M_1, M_2, M_t] predicted T_eff vs the simulated latency per committed
+    # token over 10^4 cycles agree within 10% (the continuous composition pushes the
+    # expectation through a nonlinear map, so it is not exact)
+    T = [1.0, 5.0, 40.0]
+    for a2, a3 in itertools.product((0.3, 0.6, 0.85, 0.97), repeat=2):
+        for W in (2, 4, 8):
+            pred = O.predict_chain_latency(T, [a2, a3], W, linear, ibonus)
+            mc = simulate_t_eff(T, [a2, a3], W, linear, ibonus, cycles=10_000, seed=W)
+            assert pred == pytest.approx(mc, rel=0.10), (a2, a3, W)
+
+
+def _run_mean(a, fed):
+    """E[min(G, fed)] for G = successes before the first failure of Bernoulli(a): sum over
+    the law P(acc = i) = a^i (1 - a) (i < fed), P(acc = fed) = a^fed."""
+    return sum(i * a ** i * (1 - a) for i in range(fed)) + fed * a ** fed
+
+
+@pytest.mark.parametrize("ibonus", [True, False])
+def test_eq7_exact_when_the_middle_level_is_deterministic(ibonus):
+    # alpha_2 in {0, 1} makes the number fed to the target deterministic, so Eq. 7's
+    # composition is exact: alpha_2 = 0 -> level 2 rejects the first draft and emits its
+    # correction token (fed_3 = 1, with or without the bonus: P:64); alpha_2 = 1 -> all W
+    # accepted, plus the bonus token only with the intermediate bonus (P:65)
+    T = [1.0, 5.0, 40.0]
+    for W in (1, 3, 7):
+        for a3 in (0.2, 0.5, 0.9):
+            lat = W * T[0] + T[1] + T[2]
+            t0 = O.predict_chain_latency(T, [0.0, a3], W, False, ibonus)
+            assert t0 == pytest.approx(lat / (1 + _run_mean(a3, 1)), rel=1e-12)
+            fed = W + 1 if ibonus else W
+            t1 = O.predict_chain_latency(T, [1.0, a3], W, False, ibonus)
+            assert t1 == pytest.approx(lat / (1 + _run_mean(a3, fed)), rel=1e-12)
+            mc = simulate_t_eff(T, [0.0, a3], W, False, ibonus, cycles=100_000, seed=3)
+            assert t0 == pytest.approx(mc, rel=0.02)
+
+
+def test_eq7_four_level_monte_carlo():
+    T = [1.0, 3.0, 10.0, 40.0]
+    for a in ((0.4, 0.8, 0.95), (0.9, 0.6, 0.8), (0.95, 0.95, 0.95)):
+        for ib in (True, False):
+            pred = O.predict_chain_latency(T, list(a), 6, False, ib)
+            assert pred == pytest.approx(simulate_t_eff(T, list(a), 6, False, ib, 20_000, 5), rel=0.10)
