@@ -44,23 +44,26 @@ struct RowStat {
     int32_t bad;    // NaN / +inf present or row all -inf
 };
 
-// Slice geometry of a vocabulary of V entries: C slices of VSe (<= VS) entries.  C is
-// the smallest value in [ceil(V/VS), 5/4 ceil(V/VS)] for which k = floor(148/C) groups of C
-// CTAs keep the most SMs busy (a group owns whole units, so units never straddle rounds and
-// the groups never wait on each other; see msd_core.cu).
+// Slice geometry of a vocabulary of V entries: C slices of VSe (<= VS) entries.  The core
+// kernel gives each CTA two adjacent slices (bf16) per item, so a unit occupies ceil(C / 2)
+// CTAs; C is the value in [ceil(V/VS), 5/4 ceil(V/VS)] for which k = floor(148 / ceil(C/2))
+// groups keep the most SMs busy (an even C on ties: no half-empty CTA).  A group owns whole
+// units, so units never straddle rounds and the groups never wait on each other (msd_core.cu).
 struct SliceGeom {
     int32_t C;
     int32_t VSe;
 };
 constexpr int REF_SMS = 148;   // B200
+__host__ __device__ inline int32_t geom_used_sms(int32_t c) {
+    const int32_t cc = (c + 1) / 2;
+    return (REF_SMS / cc) * cc;
+}
 __host__ __device__ inline SliceGeom slice_geometry(int64_t V) {
     const int32_t cmin = (int32_t)((V + VS - 1) / VS);
-    // the smallest C in [cmin, 5 cmin / 4] (slices stay >= 80% of VS) that keeps the most SMs
-    // busy (all 148 if possible): k = floor(148 / C) groups of C CTAs
-    int32_t best = cmin, used = (REF_SMS / cmin) * cmin;
-    for (int32_t c = cmin + 1; c <= cmin + cmin / 4 && c <= REF_SMS && used < REF_SMS; ++c) {
-        const int32_t u = (REF_SMS / c) * c;
-        if (u > used) { used = u; best = c; }
+    int32_t best = cmin, used = geom_used_sms(cmin);
+    for (int32_t c = cmin + 1; c <= cmin + cmin / 4 && c <= 2 * REF_SMS; ++c) {
+        const int32_t u = geom_used_sms(c);
+        if (u > used || (u == used && (best & 1) && !(c & 1))) { used = u; best = c; }
     }
     SliceGeom g;
     g.C = best;

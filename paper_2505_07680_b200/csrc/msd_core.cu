@@ -49,20 +49,17 @@
 
 namespace msd {
 
-constexpr int NCW = 8;                 // pass-1 warps = element regions of a slice
+constexpr int NCW = 8;                 // pass-1 warps = element regions of an item
 constexpr int NCW2 = 8;                // pass-2 warps: warp v handles regions v, v + NCW2, ...
 constexpr int NPR = NCW / NCW2;        // regions per pass-2 warp
-constexpr int CTH = NCW * 32;          // pass-1 threads
-constexpr int CET = VS / CTH;          // elements per pass-1 thread per row (16)
-constexpr int WCH = CET * 32;          // contiguous slice entries per pass-1 warp (512)
+constexpr int CET = 32;                // elements per pass-1 thread per row
+constexpr int WCH = CET * 32;          // contiguous entries per region (1024)
+constexpr int HREG = VS / WCH;         // regions per half (4): half h = tail slice 2 s + h
 constexpr int TCOLS = 256;             // TMEM columns per region (2 regions per lane quadrant)
 #ifndef MSD_NFETCH
 #define MSD_NFETCH 2
 #endif
 constexpr int NFETCH = MSD_NFETCH;
-#ifndef MSD_LDGSTS
-#define MSD_LDGSTS 0                   // 1: the producer streams with 16-byte cp.async instead of bulk copies
-#endif
 // Warp numbering: latency-critical service warps first, then pass 2, then the throughput
 // warps (pass 1).  Pass-1 warp W_P1 + r owns region r in TMEM lane quadrant r % 4; pass-2
 // warp W_P2 + v serves regions v and v + 4 (quadrant v): both bases are multiples of 4.
@@ -78,7 +75,7 @@ constexpr int FBUF = 192;              // records per fetcher staging buffer (L 
 constexpr int SMEM_BUDGET = 227 * 1024;
 constexpr int R1 = 4, R2 = 4;          // pass-1 / pass-2 record rings (powers of two)
 constexpr int NSUB = 4;                // per-warp records after a 3-step shuffle fold (lanes 0..3)
-static_assert(CET == 16, "two 16-byte bf16 vectors per thread and row");
+static_assert(NCW == 2 * HREG, "two halves of HREG regions");
 
 struct WF {                // pass-2 factors of one (row, warp) of the current slice
     float rho;             // rho = c_b S_a / (S_b c_a)  (pair ending at this row)
@@ -229,10 +226,11 @@ template <typename Tin, int L, int NV>
 __device__ __noinline__ void repair_stage(Tin* stage, int rs, const LevelDesc& lv, int64_t b, int64_t i,
                                           int64_t base, int w, int lane, int len_bulk, int len) {
     constexpr int VEC = Elem<Tin>::VEC;
+    const int hoff = (w / HREG) * VS;            // this region's half of the ring row
     for (int l = 0; l < L; ++l) {
-        Tin* sl = stage + (size_t)l * rs;
+        Tin* sl = stage + (size_t)l * rs + hoff;
         for (int jv = 0; jv < NV; ++jv) {
-            const int e0 = vec_index<Tin>(w, lane, jv);
+            const int e0 = vec_index<Tin>(w, lane, jv) - hoff;
             if (e0 + VEC <= len_bulk || e0 >= len) continue;
             const uint4 v = load_straddle<Tin>(
                 sl, reinterpret_cast<const Tin*>(lv.ptr[l]) + b * lv.bs[l] + i * lv.ld[l] + base, e0, len_bulk, len);
@@ -243,15 +241,16 @@ __device__ __noinline__ void repair_stage(Tin* stage, int rs, const LevelDesc& l
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// e = 2^((z - m) log2 e) of one thread's CET elements of one row (y = z - m returned too);
-// `clamp`: the -1e30 clamp first (-inf -> p = 0 without 0 * inf), NaN kept.
+// e = 2^((z - m) log2 e) of a 16-element chunk of one thread's elements of one row (y = z - m
+// returned too); `clamp`: the -1e30 clamp first (-inf -> p = 0 without 0 * inf), NaN kept.
+constexpr int CH = 16;
 template <typename Tin>
 __device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, float* e, float2* y) {
     const float nm = -m;
     const float2 nm2 = make_float2(nm, nm);
     const float2 l2e = make_float2(LOG2E, LOG2E);
 #pragma unroll
-    for (int pp = 0; pp < CET / 2; ++pp) {
+    for (int pp = 0; pp < CH / 2; ++pp) {
         float2 yy;
         if (sizeof(Tin) == 2) {
             uint32_t w = word_of(raw[pp >> 2], pp & 3);
@@ -278,7 +277,7 @@ __device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, f
     }
 }
 
-// e and y = z - m of half h (8 of the thread's 16 elements) of one row of a ring stage
+// e and y = z - m of quarter h (8 of the thread's 32 elements) of one row of a ring stage
 template <typename Tin>
 __device__ __forceinline__ void half_exp(const Tin* row, int rg, int lane, int h, float m, bool clamp, float* e,
                                          float2* y) {
@@ -318,7 +317,7 @@ __device__ __forceinline__ void half_exp(const Tin* row, int rg, int lane, int h
         y[pp] = yy;
     }
 }
-// element index (within the slice) of element 2 pp (+1) of half h of pass-1 thread (rg, lane)
+// ring-row index of element 2 pp (+1) of quarter h of pass-1 thread (rg, lane)
 template <typename Tin>
 __device__ __forceinline__ int half_index(int rg, int lane, int h, int pp) {
     constexpr int VEC = Elem<Tin>::VEC;
@@ -378,11 +377,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     const int RS = p.rs;                    // ring row stride (entries)
     const int S = p.stages;
     const int PP = p.pat_p, PT = p.pat_t;
-    const int nact = min(NCW, (VSe + WCH - 1) / WCH);   // element regions (pass-1 warps) with data
-    const int np2 = min(NCW2, nact);                     // pass-2 warps with data
-    // group scheduling: the grid is k groups of C CTAs; CTA (group, s) handles slice s of
-    // units group, group + k, ... -- a unit's C slices always run together on one group
-    const int kgrp = gridDim.x / C;
+    // An item is NH (2 for bf16, 1 for f32) consecutive tail slices t = NH s + h of one unit:
+    // the ring row holds them in halves of VS entries, region w (1024 entries) lies in half
+    // w / HREG.  Group scheduling: the grid is k groups of Cc = ceil(C / NH) CTAs; CTA (group, s)
+    // handles core slice s of units group, group + k, ... -- a unit's slices always run
+    // together on one group.
+    constexpr int NH = ES == 2 ? 2 : 1;
+    const int Cc = (C + NH - 1) / NH;
+    const int kgrp = gridDim.x / Cc;
     // With one CTA on every SM (1024 threads x 64 registers: never two per SM) the SM id is a
     // permutation of the CTA ids; grouping by SM id keeps a group's exchange among neighbouring
     // SMs (measured: core 1.1455 -> 1.1412 ms on Llama-3; interleaved groups 1.1444 ms)
@@ -393,30 +395,43 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsmid));
         if (nsmid == gridDim.x) vcta = (int)smid;
     }
-    const int grp = vcta / C, sfix = vcta % C;
+    const int grp = vcta / Cc, sfix = vcta % Cc;
     const int n_my = grp < kgrp && grp < p.U ? (p.U - grp + kgrp - 1) / kgrp : 0;
 
-    // this CTA's slice s = blockIdx % C is the same for all its items, so is its length: the
-    // ring tail [len_bulk, RS) of every row is never written by the bulk copies -- the pad
-    // value (~ -2.4e30) once, so every active warp loads whole vectors unconditionally (and the
-    // last slice of a row needs no second copy)
+    // this CTA's tail slices t_h = NH s + h are the same for all its items, so are their
+    // lengths: the tail [len_bulk_h, VS) of every half row is never written by the bulk copies
+    // -- the pad value (~ -2.4e30) once, so every active warp loads whole vectors
+    // unconditionally (and the last slice of a row needs no second copy)
     const int s = sfix;
-    const int64_t base = (int64_t)s * VSe;
-    const int len = (int)max((int64_t)0, min((int64_t)VSe, p.V - base));
-    const int len_bulk = (len * ES) / 16 * 16 / ES;
+    int64_t hbase[NH];
+    int hlen[NH], hbulk[NH];
+    uint32_t amask = 0;                     // bit w: region w holds data
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        const int t = NH * s + h;
+        hbase[h] = (int64_t)t * VSe;
+        hlen[h] = t < C ? (int)max((int64_t)0, min((int64_t)VSe, p.V - hbase[h])) : 0;
+        hbulk[h] = (hlen[h] * ES) / 16 * 16 / ES;
+        for (int r = 0; r < HREG; ++r)
+            if (r * WCH < hlen[h]) amask |= 1u << (h * HREG + r);
+    }
+    const int nact = __popc(amask);         // regions (pass-1 warps, pass-2 warps) with data
+    const int np2 = nact;
     {
         uint32_t* r32 = reinterpret_cast<uint32_t*>(ring);
-        const int w0 = len_bulk * ES / 4;
-        const int per_row = RS * ES / 4 - w0;
-        for (int e = tid; e < S * L * per_row; e += blockDim.x) {
-            const int row = e / per_row;
-            r32[(size_t)row * (RS * ES / 4) + w0 + (e - row * per_row)] = 0xF1F1F1F1u;
+        for (int h = 0; h < NH; ++h) {
+            const int w0 = (h * VS + hbulk[h]) * ES / 4, w1 = (h + 1) * VS * ES / 4;
+            const int per_row = w1 - w0;
+            for (int e = tid; e < S * L * per_row; e += blockDim.x) {
+                const int row = e / per_row;
+                r32[(size_t)row * (RS * ES / 4) + w0 + (e - row * per_row)] = 0xF1F1F1F1u;
+            }
         }
     }
     if (warp == W_PROD) {
         if (lane == 0) {
             // empty: one arrival per region (pass-1 warps for T items, pass-2 warps for R items)
-            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], MSD_LDGSTS ? 32 : 1); mbar_init(&c.empty[s], nact); }
+            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], nact); }
             for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], nact); mbar_init(&c.r1_empty[r], 1); }
             for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], np2); mbar_init(&c.r2_empty[r], 1); }
             for (int k = 0; k < NQ; ++k) {
@@ -438,7 +453,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 
     auto stamp = [&](int j, int k) {
 #if defined(MSD_TRACE) && !defined(MSD_PROF)
-        if (p.trace) p.trace[((int64_t)(grp + j * kgrp) * C + sfix) * 16 + k] = globaltimer();
+        if (p.trace) p.trace[((int64_t)(grp + j * kgrp) * Cc + sfix) * 16 + k] = globaltimer();
 #endif
     };
     auto item = [&](int j, int64_t& u, int64_t& b, int64_t& i) {
@@ -461,7 +476,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // keeps full relative accuracy).  Rows are processed in two 8-element halves.
         const int g1 = (warp - W_P1) / NCW;
         const int rg = (warp - W_P1) % NCW;     // element region
-        if (rg < nact) {
+        const int hh = rg / HREG;               // its half (tail slice NH s + hh)
+        const int gofs = (int)hbase[hh] - hh * VS;   // ring-row index -> vocabulary id
+        if ((amask >> rg) & 1u) {
             PROF_DECL
             const uint32_t tbase = tcol(rg);
             Cursor cu;
@@ -485,7 +502,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 PROF(0)
                 if (rg == 0 && lane == 0) stamp(j, 1);
                 // a row length that is not a multiple of 16 bytes: patch the straddling vector
-                if (len_bulk != len) repair_stage<Tin, L, NV>(stage, RS, p.lv, b, i, base, rg, lane, len_bulk, len);
+                if (hbulk[hh] != hlen[hh])
+                    repair_stage<Tin, L, NV>(stage, RS, p.lv, b, i, hbase[hh], rg, lane, hbulk[hh], hlen[hh]);
                 // per-thread then per-warp max of every row (NaN-propagating)
                 float wm[L];
 #pragma unroll
@@ -526,7 +544,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         am[l] = 0x7fffffff;
                     }
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < CET / 8; ++h) {
                         float2 yprev[4];
 #pragma unroll
                         for (int l = 0; l < L; ++l) {
@@ -553,7 +571,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                             for (int pp = 0; pp < 4; ++pp) {
                                 yprev[pp] = y[pp];
                                 if (GREEDY) {
-                                    const int ib = (int)base + half_index<Tin>(rg, lane, h, pp);
+                                    const int ib = gofs + half_index<Tin>(rg, lane, h, pp);
                                     if (y[pp].x == 0.f) am[l] = min(am[l], ib);
                                     if (y[pp].y == 0.f) am[l] = min(am[l], ib + 1);
                                 }
@@ -648,13 +666,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
     } else if (warp >= W_P2) {
         // ================================================================ pass-2 warps
-        // warp W_P2 + v handles regions v, v + NCW2, ... (same TMEM lane quadrant)
+        // warp W_P2 + v handles region v (same TMEM lane quadrant as pass-1 warp v)
+        static_assert(NPR == 1, "one region per pass-2 warp");
         const int v = warp - W_P2;
-        if (v < np2) {
+        if ((amask >> v) & 1u) {
             PROF_DECL
-            int nreg = 0;        // active regions of this warp
-#pragma unroll
-            for (int h = 0; h < NPR; ++h) nreg += (v + h * NCW2 < nact) ? 1 : 0;
             Cursor cu;
             for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
                 const int j = cu.j;
@@ -664,68 +680,58 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int r2 = j & (R2 - 1);
                 mbar_wait(&c.rowf_full[k], (uint32_t)((j / NQ) & 1));
                 PROF(0)
-                float rh[NPR][L], sc[NPR][L], wm[NPR][L];
+                float rh[L], sc[L], wm[L];
                 const uint32_t cw = c.clampw[k];
 #pragma unroll
-                for (int h = 0; h < NPR; ++h) {
-                    const int w = v + h * NCW2;
-#pragma unroll
-                    for (int l = 0; l < L; ++l) {
-                        rh[h][l] = sc[h][l] = 0.f;
-                        wm[h][l] = 0.f;
-                        if (h < nreg) {
-                            if (l > 0) {
-                                rh[h][l] = c.rowf[k][l][w].rho;
-                                sc[h][l] = c.rowf[k][l][w].scale;
-                            }
-                            wm[h][l] = c.wmx[k][l][w];
-                        }
-                    }
+                for (int l = 0; l < L; ++l) {
+                    rh[l] = l > 0 ? c.rowf[k][l][v].rho : 0.f;
+                    sc[l] = l > 0 ? c.rowf[k][l][v].scale : 0.f;
+                    wm[l] = c.wmx[k][l][v];
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&c.rowf_empty[k]);
                 float acc[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) acc[l] = 0.f;
-                // residual of the pair (l-1, l) of region h: sum max(e_l - rho e_{l-1}, 0), scaled
-                auto pair = [&](int h, int l, const float* ea, const float* eb) {
-                    const float2 nr = make_float2(-rh[h][l], -rh[h][l]);
-                    float2 a2 = make_float2(0.f, 0.f), a2b = make_float2(0.f, 0.f);
+                // residual of the pair (l-1, l) over a 16-element chunk: sum max(e_l - rho e_{l-1}, 0)
+                float2 a2[L];
 #pragma unroll
-                    for (int kk = 0; kk < CET; kk += 2) {
+                for (int l = 0; l < L; ++l) a2[l] = make_float2(0.f, 0.f);
+                auto pair = [&](int l, const float* ea, const float* eb) {
+                    const float2 nr = make_float2(-rh[l], -rh[l]);
+                    float2 x = make_float2(0.f, 0.f), xb = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int kk = 0; kk < CH; kk += 2) {
                         float2 t = __ffma2_rn(make_float2(eb[kk], eb[kk + 1]), nr, make_float2(ea[kk], ea[kk + 1]));
                         t.x = fmaxf(t.x, 0.f);
                         t.y = fmaxf(t.y, 0.f);
-                        if (kk & 2) a2b = __fadd2_rn(a2b, t);
-                        else a2 = __fadd2_rn(a2, t);
+                        if (kk & 2) xb = __fadd2_rn(xb, t);
+                        else x = __fadd2_rn(x, t);
                     }
-                    a2 = __fadd2_rn(a2, a2b);
-                    acc[l] = fmaf(a2.x + a2.y, sc[h][l], acc[l]);
+                    a2[l] = __fadd2_rn(a2[l], __fadd2_rn(x, xb));
                 };
                 if (isT) {
                     mbar_wait(&c.tm_full[q], (uint32_t)cu.tph);
                     if (v == 0 && lane == 0) stamp(j, 12);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     PROF(1)
+                    const uint32_t tb = tcol(v) + (uint32_t)(q * CET * L);
 #pragma unroll
-                    for (int h = 0; h < NPR; ++h) {
-                        if (h < nreg) {
-                            const uint32_t tb = tcol(v + h * NCW2) + (uint32_t)(q * CET * L);
-                            float ea[CET], eb[CET], ec[CET];
-                            tm_ld16(tb, eb);
-                            tm_ld16(tb + (uint32_t)CET, ea);
-                            if (L > 2) tm_ld16(tb + (uint32_t)(2 * CET), ec);
+                    for (int ch = 0; ch < CET / CH; ++ch) {
+                        float ea[CH], eb[CH], ec[CH];
+                        tm_ld16(tb + (uint32_t)(ch * CH), eb);
+                        tm_ld16(tb + (uint32_t)(CET + ch * CH), ea);
+                        if (L > 2) tm_ld16(tb + (uint32_t)(2 * CET + ch * CH), ec);
+                        tm_wait_ld();
+                        pair(1, ea, eb);
+                        if (L > 2) pair(2, ec, ea);
+#pragma unroll
+                        for (int l = 3; l < L; ++l) {
+#pragma unroll
+                            for (int kk = 0; kk < CH; ++kk) eb[kk] = ec[kk];
+                            tm_ld16(tb + (uint32_t)(l * CET + ch * CH), ec);
                             tm_wait_ld();
-                            pair(h, 1, ea, eb);
-                            if (L > 2) pair(h, 2, ec, ea);
-#pragma unroll
-                            for (int l = 3; l < L; ++l) {
-#pragma unroll
-                                for (int kk = 0; kk < CET; ++kk) eb[kk] = ec[kk];
-                                tm_ld16(tb + (uint32_t)(l * CET), ec);
-                                tm_wait_ld();
-                                pair(h, l, ec, eb);
-                            }
+                            pair(l, ec, eb);
                         }
                     }
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -740,31 +746,34 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     PROF(1)
                     const Tin* stage = ring + (size_t)cu.st * L * RS;
                     const bool skip_r = (p.dbg & 2) != 0;   // debug: R items skip the recomputation
+                    if (!skip_r) {
+                        const bool clamp = ((cw >> v) & 1u) || ES == 4;
+                        constexpr int NVC = CH / VEC;      // vectors per chunk
 #pragma unroll
-                    for (int h = 0; h < NPR; ++h) {
-                        if (h < nreg && !skip_r) {
-                            const int w = v + h * NCW2;
-                            const bool clamp = ((cw >> w) & 1u) || ES == 4;
-                            float eprev[CET];
+                        for (int ch = 0; ch < CET / CH; ++ch) {
+                            float eprev[CH];
 #pragma unroll
                             for (int l = 0; l < L; ++l) {
-                                uint4 raw[NV];
+                                uint4 raw[NVC];
 #pragma unroll
-                                for (int jv = 0; jv < NV; ++jv)
-                                    raw[jv] = *reinterpret_cast<const uint4*>(stage + (size_t)l * RS + vec_index<Tin>(w, lane, jv));
-                                float e[CET];
-                                float2 y[CET / 2];
-                                row_exp<Tin>(raw, wm[h][l], clamp, e, y);
-                                if (l > 0) pair(h, l, e, eprev);
+                                for (int jv = 0; jv < NVC; ++jv)
+                                    raw[jv] = *reinterpret_cast<const uint4*>(stage + (size_t)l * RS +
+                                                                              vec_index<Tin>(v, lane, ch * NVC + jv));
+                                float e[CH];
+                                float2 y[CH / 2];
+                                row_exp<Tin>(raw, wm[l], clamp, e, y);
+                                if (l > 0) pair(l, e, eprev);
 #pragma unroll
-                                for (int kk = 0; kk < CET; ++kk) eprev[kk] = e[kk];
+                                for (int kk = 0; kk < CH; ++kk) eprev[kk] = e[kk];
                             }
                         }
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cnt(&c.empty[cu.st], (uint32_t)nreg);
+                    if (lane == 0) mbar_arrive(&c.empty[cu.st]);
                     PROF(2)
                 }
+#pragma unroll
+                for (int l = 1; l < L; ++l) acc[l] = (a2[l].x + a2[l].y) * sc[l];
 #pragma unroll
                 for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
                 PROF(3)
@@ -784,38 +793,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     } else if (warp == W_PROD) {
         // ================================================================ TMA producer
         PROF_DECL
-#if MSD_LDGSTS
-        // the whole warp issues 16-byte cp.async (LDGSTS) copies; each lane's copies complete
-        // on the stage's full barrier (count 32, arrive.noinc)
-        {
-            const uint64_t pol = policy_evict_first();
-            const int nvec = len_bulk * ES / 16;
-            Cursor cu;
-            for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
-                const int j = cu.j;
-                if (j >= S) mbar_wait(&c.empty[cu.st], (uint32_t)(cu.sph ^ 1));
-                int64_t u, b, i;
-                item(j, u, b, i);
-#pragma unroll
-                for (int l = 0; l < L; ++l) {
-                    const uint32_t dst = smem_u32(ring + ((size_t)cu.st * L + l) * RS);
-                    const char* src = reinterpret_cast<const char*>(reinterpret_cast<const Tin*>(p.lv.ptr[l]) +
-                                                                    b * p.lv.bs[l] + i * p.lv.ld[l] + base);
-                    for (int x = lane; x < nvec; x += 32)
-                        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst + 16 * x),
-                                     "l"(src + 16 * (size_t)x), "l"(pol)
-                                     : "memory");
-                }
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&c.full[cu.st]))
-                             : "memory");
-            }
-        }
-        if (false) {
-#else
         if (lane == 0) {
-#endif
             const uint64_t pol = policy_evict_first();
-            const uint32_t bytes = (uint32_t)(len_bulk * ES);   // [len_bulk, RS) holds the pad
+            uint32_t hb[NH], bytes = 0;              // [hbulk_h, VS) of each half holds the pad
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                hb[h] = (uint32_t)(hbulk[h] * ES);
+                bytes += hb[h];
+            }
             Cursor cu;
             for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
                 const int j = cu.j;
@@ -829,8 +814,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         Tin* dst = ring + ((size_t)cu.st * L + l) * RS;
-                        const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] + i * p.lv.ld[l] + base;
-                        bulk_g2s(dst, src, bytes, &c.full[cu.st], pol);
+                        const Tin* src = reinterpret_cast<const Tin*>(p.lv.ptr[l]) + b * p.lv.bs[l] + i * p.lv.ld[l];
+#pragma unroll
+                        for (int h = 0; h < NH; ++h)
+                            if (hb[h]) bulk_g2s(dst + h * VS, src + hbase[h], hb[h], &c.full[cu.st], pol);
                     }
                 } else {
                     mbar_arrive(&c.full[cu.st]);   // nothing to copy (a slice past the row end)
@@ -843,13 +830,15 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     } else if (warp == W_PUB) {
         // ================================================================ publisher
         // lane = 8 l + w: row l, region w (L <= 4).  Each lane sums its region's sub-records,
-        // scales them by 2^((m_w - m_s) log2 e) relative to the slice maximum m_s (1 when the
-        // region holds the maximum) and the row's 8 lanes reduce with 3 shuffle levels.
-        static_assert(NCW == 8 && L * NCW <= 32, "publisher lane layout");
+        // scales them by 2^((m_w - m_s) log2 e) relative to the tail slice's maximum m_s (1 when
+        // the region holds the maximum) and the HREG lanes of each half reduce with 2 shuffle
+        // levels: one record per (row, tail slice NH s + w / HREG).
+        static_assert(NCW == 8 && HREG == 4 && L * NCW <= 32, "publisher lane layout");
         PROF_DECL
         const int l = lane >> 3, w = lane & 7;
         const bool inrow = l < L;
-        const bool act = inrow && w < nact;
+        const bool act = inrow && ((amask >> w) & 1u);
+        const int tslice = NH * s + w / HREG;   // this lane's tail slice
         for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             item(j, u, b, i);
@@ -870,10 +859,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
             PROF(2)
-            // slice maximum of the row (NaN-propagating) over the row's 8 lanes
+            // tail-slice maximum of the row (NaN-propagating) over the half's HREG lanes
             float msl = wm;
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
+            for (int o = HREG / 2; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
             float f = wm == msl ? 1.f : ex2f((wm - msl) * LOG2E);
             if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
             // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
@@ -881,17 +870,17 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             int ax = (wm == msl) ? aw : 0x7fffffff;
             PROF(3)
 #pragma unroll
-            for (int o = 4; o > 0; o >>= 1) {
+            for (int o = HREG / 2; o > 0; o >>= 1) {
                 Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
                 Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
                 if (GREEDY) ax = min(ax, __shfl_xor_sync(0xffffffffu, ax, o));
             }
             PROF(4)
-            // lane 8 l publishes row l: first the self-validating exchange record (the other
-            // slices wait for it; sum != 0: the slice maximum's entry has e = 1 in the sum),
-            // then the Partial for the tail
-            if (inrow && w == 0) {
-                const size_t idx = ((size_t)u * L + l) * C + s;
+            // lanes 8 l and 8 l + HREG publish row l's records of the two tail slices: first the
+            // self-validating exchange record (the other slices wait for it; sum != 0: the slice
+            // maximum's entry has e = 1 in the sum), then the Partial for the tail
+            if (inrow && (w % HREG) == 0 && w / HREG < NH && tslice < C) {
+                const size_t idx = ((size_t)u * L + l) * C + tslice;
                 st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
                                ((unsigned long long)__float_as_uint(Sx) << 32) | __float_as_uint(msl));
                 Partial pr;
@@ -963,7 +952,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             float Rl[L], Sl[L];
 #pragma unroll
             for (int l = 0; l < L; ++l) {
-                Rl[l] = __uint_as_float((uint32_t)fb[l * C + s]);
+                Rl[l] = __uint_as_float((uint32_t)fb[l * C + NH * s]);   // first tail slice's record
                 Sl[l] = 0.f;
             }
             for (int t = lane; t < C; t += 32) {
@@ -1013,7 +1002,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             // per-region factors: x = NCW (l - 1) + w for region w and the pair ending at row l
             for (int x = lane; x < (L - 1) * NCW; x += 32) {
                 const int w = x % NCW, l = 1 + x / NCW;
-                if (w < nact) {
+                if ((amask >> w) & 1u) {
                     float Ma = Rl[0], Mb = Rl[0], Sa = Sl[0], Sb = Sl[0];
 #pragma unroll
                     for (int r = 1; r < L; ++r)
@@ -1044,8 +1033,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     } else if (warp == W_RED) {
         // ================================================================ reducer (slice residual)
         PROF_DECL
+        // lane = 4 v + t: region v (half v / HREG), sub-record t; each half's 16 lanes fold
+        static_assert(NCW2 * NSUB == 32 && HREG * NSUB == 16, "reducer lane layout");
         const int v = lane >> 2, t = lane & 3;
-        const bool act = v < np2;
+        const bool act = (amask >> v) & 1u;
+        const int tslice = NH * s + v / HREG;
         for (int j = 0; j < n_my; ++j) {
             int64_t u, b, i;
             item(j, u, b, i);
@@ -1057,17 +1049,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             for (int l = 1; l < L; ++l) {
                 float d = act ? c.r2R[r2][l][v][t] : 0.f;
 #pragma unroll
-                for (int o = NCW2 * NSUB / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                for (int o = HREG * NSUB / 2; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
                 R[l] = d;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&c.r2_empty[r2]);
-            if (lane >= 1 && lane < L) {
-                float x = R[1];
+            if ((lane % (HREG * NSUB)) == 0 && lane / (HREG * NSUB) < NH && tslice < C) {
 #pragma unroll
-                for (int l = 2; l < L; ++l)
-                    if (lane == l) x = R[l];
-                p.resid[((size_t)u * (L - 1) + (lane - 1)) * C + s] = f2d_alu(x);
+                for (int l = 1; l < L; ++l) p.resid[((size_t)u * (L - 1) + (l - 1)) * C + tslice] = f2d_alu(R[l]);
             }
             if (lane == 0) stamp(j, 15);
             PROF(1)
@@ -1092,8 +1081,8 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     CoreParams p = p0;
     const int ES = (int)sizeof(Tin);
     const int NT = core_tslots(L);
-    const int nact = std::min(NCW, (p.VSe + WCH - 1) / WCH);
-    p.rs = nact * WCH;
+    const int NH = ES == 2 ? 2 : 1;          // tail slices per item
+    p.rs = NH * VS;
     const size_t ctl = align_up(sizeof(Ctl<L>), 128);
     const size_t stage_bytes = (size_t)L * p.rs * ES;
     int S = (int)((SMEM_BUDGET - ctl - 256) / stage_bytes);
@@ -1103,9 +1092,7 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     // item pattern: T items use the NT TMEM slots; R items keep their ring stage.  Of the S
     // stages ~4 are needed in flight for the TMA; the rest may hold R items.
     int pt = env_int("MSD_PAT_T", NT), pr = env_int("MSD_PAT_R", -1);
-    // measured on B200 (tools/core_sweep.py, Llama-3): 2 kept-ring items per 5 TMEM items is
-    // best; more R items cost MUFU recomputation, fewer leave the exchange latency exposed
-    if (pr < 0) pr = std::max(0, std::min(2, S - 5));
+    if (pr < 0) pr = std::max(0, std::min(2, S - 3));
     if (pt < 1) pt = 1;
     p.pat_t = pt;
     p.pat_p = pt + pr;
@@ -1120,11 +1107,13 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     if (L * p.C > FBUF) return cudaErrorInvalidValue;   // vocabulary too large for the exchange buffer
-    // one CTA per SM (it owns all 512 TMEM columns); k = floor(nsm / C) groups of C CTAs
-    int64_t kg = nsm / p.C;
+    // one CTA per SM (it owns all 512 TMEM columns); k = floor(nsm / Cc) groups of
+    // Cc = ceil(C / NH) CTAs
+    const int Cc = (p.C + NH - 1) / NH;
+    int64_t kg = nsm / Cc;
     if (kg < 1) return cudaErrorInvalidConfiguration;
     if (kg > p.U) kg = p.U;
-    const int64_t grid = kg * p.C;
+    const int64_t grid = kg * Cc;
     void* args[] = {&p};
     return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(CORE_THREADS), args, smem, s);
 }

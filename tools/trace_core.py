@@ -9,21 +9,21 @@ c = synth.CONFIGS[name]
 inp = synth.gauss_chain(c["B"], c["V"], c["K"], c["L"], c["sigmas"], s=c["s"], seed=c["seed"], device="cuda", dtype=c["dtype"])
 cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"])
 def geo(V, VS=4096, REF=148):
-    cmin = (V + VS - 1) // VS; best = cmin; used = (REF // cmin) * cmin; cc = cmin + 1
-    while cc <= cmin + cmin // 4 and cc <= REF and used < REF:
-        u = (REF // cc) * cc
-        if u > used: used = u; best = cc
-        cc += 1
-    return best
+    """core slices per unit: ceil(C / 2) CTAs for the tail's C slices (msd_common.cuh)"""
+    used = lambda cc: (REF // ((cc + 1) // 2)) * ((cc + 1) // 2)
+    cmin = (V + VS - 1) // VS; best = cmin; u0 = used(cmin)
+    for cc in range(cmin + 1, cmin + cmin // 4 + 1):
+        if used(cc) > u0 or (used(cc) == u0 and best % 2 and not cc % 2): u0 = used(cc); best = cc
+    return (best + 1) // 2 if c["dtype"] == "bf16" else best
 C = geo(c["V"])
 n_items = c["B"] * c["K"] * C
-buf = torch.zeros(n_items * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(n_items * 2 * 16 + 16, dtype=torch.int64, device="cuda")   # >= units x tail slices
 lib = api.lib(); lib.msd_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 cv(); torch.cuda.synchronize()
 lib.msd_debug_set_trace(buf.data_ptr(), buf.numel() * 8)
 cv(); torch.cuda.synchronize()
 lib.msd_debug_set_trace(None, 0)
-t = buf.view(n_items, 16).cpu().numpy().astype(np.float64)
+t = buf[:n_items * 16].view(n_items, 16).cpu().numpy().astype(np.float64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan) / 1e3   # us
 N = ["tma", "p1.full", "p1.tmE", "p1.end", "f.loads", "pub.done", "f.start", "f.cnt", "f.comb", "f.rowfE",
