@@ -57,7 +57,10 @@ constexpr int WCH = CET * 32;          // contiguous entries per region (1024)
 constexpr int HREG = VS / WCH;         // regions per half (4): half h = tail slice 2 s + h
 constexpr int TCOLS = 256;             // TMEM columns per region (2 regions per lane quadrant)
 #ifndef MSD_NFETCH
-#define MSD_NFETCH 2
+#define MSD_NFETCH 1
+#endif
+#ifndef MSD_POLL_NS
+#define MSD_POLL_NS 64                 // fetcher back-off between polls of the exchange records
 #endif
 constexpr int NFETCH = MSD_NFETCH;
 // Warp numbering: latency-critical service warps first, then pass 2, then the throughput
@@ -127,6 +130,20 @@ __device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
           "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
         : "r"(ta));
 }
+#ifndef MSD_SPIN_SERVICE
+#define MSD_SPIN_SERVICE 1
+#endif
+// latency-critical waits (publisher, fetchers, reducer, pass 2): a spinning probe, so the warp
+// resumes as soon as the phase completes instead of after a suspended try_wait wakes it
+__device__ __forceinline__ void mbar_wait_lat(uint64_t* bar, uint32_t parity) {
+#if MSD_SPIN_SERVICE
+    while (!mbar_try_wait(bar, parity)) {
+    }
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 // non-blocking probe of a phase (no suspend)
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done;
@@ -678,7 +695,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int q = cu.q;
                 const int k = j & (NQ - 1);
                 const int r2 = j & (R2 - 1);
-                mbar_wait(&c.rowf_full[k], (uint32_t)((j / NQ) & 1));
+                mbar_wait_lat(&c.rowf_full[k], (uint32_t)((j / NQ) & 1));
                 PROF(0)
                 float rh[L], sc[L], wm[L];
                 const uint32_t cw = c.clampw[k];
@@ -711,7 +728,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     a2[l] = __fadd2_rn(a2[l], __fadd2_rn(x, xb));
                 };
                 if (isT) {
-                    mbar_wait(&c.tm_full[q], (uint32_t)cu.tph);
+                    mbar_wait_lat(&c.tm_full[q], (uint32_t)cu.tph);
                     if (v == 0 && lane == 0) stamp(j, 12);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     PROF(1)
@@ -844,7 +861,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             item(j, u, b, i);
             const int k = j & (NQ - 1);
             const int r1 = j & (R1 - 1);
-            mbar_wait(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
+            mbar_wait_lat(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
             PROF(0)
             float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
             int aw = 0x7fffffff;
@@ -912,7 +929,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             if (lane == 0) stamp(j, 6);
             // the other slices of the unit are published around the time this one is: poll only
             // from then on (polls steal issue slots and L2 bandwidth)
-            mbar_wait(&c.pub[k], (uint32_t)((j / NQ) & 1));
+            mbar_wait_lat(&c.pub[k], (uint32_t)((j / NQ) & 1));
             const uint64_t t0 = globaltimer();
             PROF(4)
             // stage the unit's records; a record whose sum is still 0 is not yet visible
@@ -941,7 +958,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     }
                     break;
                 }
-                __nanosleep(64);
+                __nanosleep(MSD_POLL_NS);
             }
             __syncwarp();
             if (lane == 0) stamp(j, 4);
@@ -1042,7 +1059,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             int64_t u, b, i;
             item(j, u, b, i);
             const int r2 = j & (R2 - 1);
-            mbar_wait(&c.r2_full[r2], (uint32_t)((j / R2) & 1));
+            mbar_wait_lat(&c.r2_full[r2], (uint32_t)((j / R2) & 1));
             PROF(0)
             float R[L];
 #pragma unroll
