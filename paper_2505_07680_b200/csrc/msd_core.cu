@@ -671,6 +671,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 }
                 __syncwarp();
                 if (rg == 0 && lane == 0) stamp(j, 3);
+#if defined(MSD_TRACE) && !defined(MSD_PROF)
+                if (lane == 0 && p.trace)
+                    atomicMax(p.trace + ((int64_t)(grp + j * kgrp) * Cc + sfix) * 16 + 7, (unsigned long long)globaltimer());
+#endif
                 if (lane == 0 && !p1only) {
                     mbar_arrive(&c.r1_full[r1]);
                     if (isT) mbar_arrive(&c.tm_full[q]);
@@ -862,6 +866,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             const int k = j & (NQ - 1);
             const int r1 = j & (R1 - 1);
             mbar_wait_lat(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
+            if (lane == 0) stamp(j, 8);
             PROF(0)
             float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
             int aw = 0x7fffffff;
@@ -893,6 +898,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 if (GREEDY) ax = min(ax, __shfl_xor_sync(0xffffffffu, ax, o));
             }
             PROF(4)
+            if (lane == 0) stamp(j, 9);
             // lanes 8 l and 8 l + HREG publish row l's records of the two tail slices: first the
             // self-validating exchange record (the other slices wait for it; sum != 0: the slice
             // maximum's entry has e = 1 in the sum), then the Partial for the tail

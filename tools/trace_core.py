@@ -26,13 +26,13 @@ lib.msd_debug_set_trace(None, 0)
 t = buf[:n_items * 16].view(n_items, 16).cpu().numpy().astype(np.float64)
 t0 = t[t > 0].min()
 t = np.where(t > 0, t - t0, np.nan) / 1e3   # us
-N = ["tma", "p1.full", "p1.tmE", "p1.end", "f.loads", "pub.done", "f.start", "f.cnt", "f.comb", "f.rowfE",
+N = ["tma", "p1.full", "p1.tmE", "p1.end", "f.loads", "pub.done", "f.start", "p1.last", "pub.wake", "pub.calc",
      "f.done", "p2.rowf", "p2.tmF", "p2.end", "red.r2", "red.end"]
 print("kernel span us %.1f" % np.nanmax(t))
 def d(a, b):
     x = t[:, b] - t[:, a]
     return f"{N[a]:>8} -> {N[b]:<8} med {np.nanmedian(x):7.2f} p90 {np.nanpercentile(x, 90):7.2f}"
-for a, b in [(0, 1), (1, 2), (2, 3), (3, 5), (6, 4), (4, 10), (10, 12), (3, 12), (12, 13), (13, 15), (5, 4)]:
+for a, b in [(0, 1), (1, 2), (2, 3), (3, 7), (7, 8), (8, 9), (9, 5), (3, 5), (6, 4), (4, 10), (10, 12), (3, 12), (12, 13), (13, 15), (5, 4)]:
     print(d(a, b))
 U = n_items // C
 pub = t[:, 5].reshape(U, C)
