@@ -112,8 +112,11 @@ typedef struct {
  *    c[0:n] ++ [y] (pad -1); out_len[B]; pos_dtv/pos_kl[B][K] (or NULL): DTV(p_i,q_i)
  *    (Eq. 5) and KL(p_i || q_i) in nats at every position i < K; stats (or NULL):
  *    one msd_pair_stats, +=; flags[B]: OR-ed MSD_F_* bits (required).
- * ws: device workspace of >= msd_verify_level_workspace(B, K, V) bytes, zero-filled
- *    before its first use and not modified by the caller afterwards.
+ * ws: device workspace of >= msd_verify_level_workspace(B, K, V) bytes (256-byte aligned), not
+ *    modified by the caller between calls.  Its layout depends on (B, K, V): the library zeroes
+ *    the exchange-record region (on `stream`) whenever a workspace is used with a shape other
+ *    than its previous one, or for the first time, so one maximal workspace may serve calls of
+ *    different shapes; calls sharing a workspace must not run concurrently.
  * ------------------------------------------------------------------------- */
 msd_status msd_verify_level(msd_logits q, msd_logits p, int32_t B, int32_t K, int64_t V,
                             const int32_t* cand, const int32_t* m,
@@ -146,7 +149,7 @@ size_t msd_verify_level_workspace(int32_t B, int32_t K, int64_t V);
  *    pos_dtv, pos_kl [L-1][B][K] (NULL ok): Eq. 5 DTV and KL(p_l || p_{l-1}) at
  *      every draft position, for every adjacent pair (SimScore input, Eq. 6);
  *    stats[L-1] (NULL ok): per-pair msd_pair_stats, +=;  flags[B]: required.
- * ws: >= msd_chain_verify_workspace(L, B, K, V) bytes, zero-filled before first use.
+ * ws: >= msd_chain_verify_workspace(L, B, K, V) bytes; same contract as msd_verify_level's.
  * Equivalence: identical to L-1 sequential msd_verify_level calls where level l's q
  *    rows are level l-1's p rows (tokens, lengths, per-position divergence at i < K).
  * ------------------------------------------------------------------------- */
@@ -171,8 +174,8 @@ size_t msd_chain_verify_workspace(int32_t L, int32_t B, int32_t K, int64_t V);
  * rollback[n_models][B] (device int32): r_b per model (msd_chain_verify output).
  * Per model and request: new = seq_len - r; blocks j in [ceil(new/bs), ceil(old/bs))
  *    are pushed on the free stack in request-major, ascending-j order and their
- *    table entries set to -1.  r < 0 or r > seq_len: request untouched,
- *    MSD_F_ROLLBACK_OVF.  If a model's released blocks would overflow free_cap,
+ *    table entries set to -1.  r < 0, r > seq_len, or seq_len > max_blocks * block_size
+ *    (the request's block-table row cannot hold it): request untouched, MSD_F_ROLLBACK_OVF.  If a model's released blocks would overflow free_cap,
  *    none of its blocks are released (seq_len still shrinks), MSD_F_FREELIST_OVF.
  * flags[B] (device): OR-ed.
  * ------------------------------------------------------------------------- */
@@ -268,11 +271,25 @@ msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, i
  * ------------------------------------------------------------------------- */
 const char* msd_last_error(void);
 int32_t msd_abi_version(void);
+/* msd_init: one-time setup of the current device (the float64 exp table of the exact draws,
+ * filled on a private stream that is waited for).  Called lazily by the first verify call;
+ * call it explicitly before capturing verify calls into a CUDA graph.  Host-synchronous. */
+msd_status msd_init(void);
 msd_status msd_prof_enable(int32_t on);
 msd_status msd_prof_read(double* core_ms, int32_t* core_launches, int32_t* total_launches);
 /* msd_debug_set_trace: device buffer of 128 bytes per core item (unit x slice) receiving 16
  * globaltimer stamps of the pipeline stages of each item (NULL disables).  Debug only. */
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes);
+/* msd_debug_set_knobs: process-wide test / diagnostic overrides of internal choices (the library
+ * reads no environment variables).  pat_t / pat_r: core item pattern (TMEM-parked items, ring-
+ * kept items per period; -1 = default); stages: TMA ring depth (-1 = default); core_dbg: core
+ * isolation mode (0 = normal; 1 = pass 1 + ring only, results invalid; 4|1 = ring only);
+ * exact_draws: 1 = every residual / bonus draw takes the float64 exact path; z_safe: residual
+ * mass below which a draw takes the exact path (default 0.05, R4; < 0 = default).
+ * The outputs are identical for every pattern / stage choice and for exact_draws 0 / 1 outside
+ * the documented near-tie bands.  Not thread-safe against concurrent calls. */
+msd_status msd_debug_set_knobs(int32_t pat_t, int32_t pat_r, int32_t stages, int32_t core_dbg,
+                               int32_t exact_draws, double z_safe);
 
 #ifdef __cplusplus
 }

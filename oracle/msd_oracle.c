@@ -354,7 +354,13 @@ void or_rollback_paged(int32_t* seq_len, int32_t* block_table, int32_t B, int32_
     int32_t* newlen = (int32_t*)malloc(sizeof(int32_t) * (size_t)(B > 0 ? B : 1));
     for (int32_t b = 0; b < B; ++b) {
         int32_t old = seq_len[b];
-        if (r[b] < 0 || r[b] > old) { if (flags) flags[b] |= OR_F_ROLLBACK_OVF; newlen[b] = old; continue; }
+        /* DESIGN.md R22: r < 0, r > seq_len, or seq_len beyond the block-table row (an
+         * inconsistent caller state) -> request untouched + ROLLBACK_OVF */
+        if (r[b] < 0 || r[b] > old || (int64_t)old > (int64_t)max_blocks * bs) {
+            if (flags) flags[b] |= OR_F_ROLLBACK_OVF;
+            newlen[b] = old;
+            continue;
+        }
         newlen[b] = old - r[b];
         int32_t j0 = (newlen[b] + bs - 1) / bs, j1 = (old + bs - 1) / bs;
         total += (j1 - j0);

@@ -89,10 +89,14 @@ def lib() -> ctypes.CDLL:
     L.msd_last_error.restype = ctypes.c_char_p
     L.msd_last_error.argtypes = []
     L.msd_abi_version.restype = i32
+    L.msd_init.restype = i32
+    L.msd_init.argtypes = []
     L.msd_prof_enable.restype = i32
     L.msd_prof_enable.argtypes = [i32]
     L.msd_prof_read.restype = i32
     L.msd_prof_read.argtypes = [P, P, P]
+    L.msd_debug_set_knobs.restype = i32
+    L.msd_debug_set_knobs.argtypes = [i32, i32, i32, i32, i32, d]
     _lib = L
     return L
 
@@ -147,6 +151,7 @@ class ChainVerify:
                  draft_fed: Optional[int] = None, pos_outputs=True, rollback=True, stats=True,
                  ws: Optional[torch.Tensor] = None):
         dev = draft.device
+        _check(lib().msd_init(), "msd_init")   # one-time device setup, outside any graph capture
         self.L = len(levels)
         self.B, self.K = draft.shape
         self.V = levels[0].shape[2] if V is None else V
@@ -326,6 +331,13 @@ def select_chain(T, sim, W, max_len=4, verify_cost=0, intermediate_bonus=True):
 def simscore_update(sim: float, stats_row, weight: float, first: bool = False) -> float:
     s = msd_pair_stats(*[int(x) for x in stats_row])
     return float(lib().msd_simscore_update(float(sim), ctypes.byref(s), float(weight), int(first)))
+
+
+def debug_knobs(pat_t=-1, pat_r=-1, stages=-1, core_dbg=0, exact_draws=False, z_safe=-1.0):
+    """Test / diagnostic overrides of internal choices (msd_debug_set_knobs); call with no
+    arguments to restore the release defaults."""
+    _check(lib().msd_debug_set_knobs(int(pat_t), int(pat_r), int(stages), int(core_dbg),
+                                     int(bool(exact_draws)), float(z_safe)), "msd_debug_set_knobs")
 
 
 def prof_enable(on=True):

@@ -16,6 +16,10 @@
 
 using namespace msd;
 
+namespace msd {
+DebugKnobs g_knobs;
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -53,9 +57,41 @@ msd_status check_arch() {
     return MSD_OK;
 }
 
-double env_double(const char* name, double dflt) {
-    const char* v = getenv(name);
-    return v ? atof(v) : dflt;
+
+// One-time per-device setup (the bf16 exp table of the tail's exact draws), under call_once:
+// on a private stream with a wait on that stream only, so it must not run while another stream
+// of the process is being captured into a CUDA graph -- call msd_init first in that case.
+msd_status device_init() {
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    static std::once_flag once[64];
+    static cudaError_t res[64];
+    if (dev < 0 || dev >= 64) return fail(MSD_E_ARCH, "device index %d", dev);
+    std::call_once(once[dev], [&]() {
+        const double* t = nullptr;
+        res[dev] = exp_table(&t, 1);
+    });
+    if (res[dev] != cudaSuccess) return cuda_fail(res[dev], "msd_init");
+    return MSD_OK;
+}
+
+// Workspace binding: the exchange records of a workspace are laid out for one (L, B, K, V);
+// a workspace seen with another shape (or for the first time) gets its record region zeroed
+// on the call's stream before use (msd.h workspace contract).
+std::mutex g_ws_mu;
+std::vector<std::pair<const void*, uint64_t>> g_ws_shape;
+bool ws_shape_changed(const void* ws, uint64_t key) {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    for (auto& e : g_ws_shape)
+        if (e.first == ws) {
+            const bool ch = e.second != key;
+            e.second = key;
+            return ch;
+        }
+    if (g_ws_shape.size() >= 256) g_ws_shape.erase(g_ws_shape.begin());
+    g_ws_shape.emplace_back(ws, key);
+    return true;
 }
 
 unsigned long long* g_trace = nullptr;   // debug trace buffer (msd_debug_set_trace)
@@ -130,6 +166,13 @@ msd_status run_engine(const Engine& E) {
         return fail(MSD_E_WORKSPACE, "workspace %zu bytes < required %zu", E.ws_bytes, w.total);
     if (((uintptr_t)E.ws) % 256) return fail(MSD_E_WORKSPACE, "workspace must be 256-byte aligned");
     char* ws = reinterpret_cast<char*>(E.ws);
+    {
+        const uint64_t key = ((uint64_t)E.L << 60) ^ ((uint64_t)E.B << 40) ^ ((uint64_t)E.K << 32) ^ (uint64_t)E.V;
+        if (ws_shape_changed(E.ws, key)) {
+            cudaError_t me = cudaMemsetAsync(ws + w.partms, 0, w.rowstat - w.partms, E.stream);
+            if (me != cudaSuccess) return cuda_fail(me, "workspace reset");
+        }
+    }
 
     CoreParams cp;
     memset(&cp, 0, sizeof(cp));
@@ -149,11 +192,7 @@ msd_status run_engine(const Engine& E) {
     cp.flags = E.flags;
     cp.err = reinterpret_cast<uint32_t*>(ws + w.hdr);
     cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
-    cp.dbg = (int32_t)env_double("MSD_CORE_DBG", 0.0);
-    {
-        cudaError_t pe = core_pad(&cp.pad);
-        if (pe != cudaSuccess) return cuda_fail(pe, "pad buffer");
-    }
+    cp.dbg = g_knobs.core_dbg;
 
     TailParams tp;
     memset(&tp, 0, sizeof(tp));
@@ -168,10 +207,12 @@ msd_status run_engine(const Engine& E) {
     tp.pos_dtv = E.pos_dtv; tp.pos_kl = E.pos_kl; tp.stats = E.stats; tp.flags = E.flags;
     tp.partials = cp.partials; tp.partms = cp.partms; tp.resid = cp.resid;
     tp.cnt = cp.cnt;
-    tp.z_safe = env_double("MSD_Z_SAFE", 0.05);   // exact draws below this residual mass (R4)
-    tp.exact_all = (int32_t)env_double("MSD_EXACT_DRAWS", 0.0);
+    tp.z_safe = g_knobs.z_safe;                  // exact draws below this residual mass (R4)
+    tp.exact_all = g_knobs.exact_draws;
     {
-        cudaError_t te = exp_table(&tp.exptab);
+        msd_status is = device_init();
+        if (is != MSD_OK) return is;
+        cudaError_t te = exp_table(&tp.exptab, 0);
         if (te != cudaSuccess) return cuda_fail(te, "exp table");
     }
 
@@ -201,6 +242,12 @@ msd_status run_engine(const Engine& E) {
 extern "C" {
 
 const char* msd_last_error(void) { return g_err.c_str(); }
+
+msd_status msd_init(void) {
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    return device_init();
+}
 int32_t msd_abi_version(void) { return MSD_ABI_VERSION; }
 
 size_t msd_chain_verify_workspace(int32_t L, int32_t B, int32_t K, int64_t V) {
@@ -268,6 +315,8 @@ msd_status msd_verify_level(msd_logits q, msd_logits p, int32_t B, int32_t K, in
                             uint32_t* flags, void* ws, size_t ws_bytes, void* stream) {
     if (B < 0 || K < 1 || K + 2 > MAXC) return fail(MSD_E_ARG, "bad B=%d / K=%d (need K <= 30)", B, K);
     if (V < 1 || V > (int64_t)128 * VS) return fail(MSD_E_ARG, "V=%lld outside [1, 524288]", (long long)V);
+    if ((int64_t)2 * slice_geometry(V).C > 192)
+        return fail(MSD_E_ARG, "2 * slices = 2 * %d exceeds 192 (vocabulary too large)", slice_geometry(V).C);
     if (mode != MSD_STOCHASTIC && mode != MSD_GREEDY) return fail(MSD_E_ARG, "unknown mode %d", mode);
     if (B == 0) return MSD_OK;
     if (!cand || !out_tok || !out_len || !flags || !n_acc)
@@ -390,6 +439,17 @@ msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, i
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes) {
     g_trace = reinterpret_cast<unsigned long long*>(dev_buf);
     g_trace_items = dev_buf ? bytes / 128 : 0;
+    return MSD_OK;
+}
+
+msd_status msd_debug_set_knobs(int32_t pat_t, int32_t pat_r, int32_t stages, int32_t core_dbg,
+                               int32_t exact_draws, double z_safe) {
+    g_knobs.pat_t = pat_t;
+    g_knobs.pat_r = pat_r;
+    g_knobs.stages = stages;
+    g_knobs.core_dbg = core_dbg;
+    g_knobs.exact_draws = exact_draws ? 1 : 0;
+    g_knobs.z_safe = z_safe >= 0 ? z_safe : 0.05;
     return MSD_OK;
 }
 

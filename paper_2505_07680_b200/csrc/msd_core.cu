@@ -4,43 +4,43 @@
 // hot path, for all L chain levels at once so every logit byte is read from HBM
 // exactly once.
 //
-// Decomposition.  A *unit* is one (request b, draft position i < K) and owns the L
-// rows Z_l[b, i, :].  A unit is cut into C slices of VSe <= VS = 4096 vocabulary
-// entries; an *item* is (unit, slice).  The kernel is persistent and cooperative (one
-// CTA per SM) and runs k = floor(148 / C) groups of C CTAs: CTA (g, s) processes slice s
-// of units g, g + k, ..., so the C items of a unit run concurrently on C SMs, which
-// exchange per-slice (max, sum) records through global memory.
+// Decomposition.  A *unit* is one (request b, draft position i < K) and owns the L rows
+// Z_l[b, i, :].  The vocabulary is cut into C tail slices of VSe <= VS = 4096 entries (the
+// granularity of the records the tail kernel combines and rescans); an *item* is one unit's
+// NH = 2 adjacent tail slices (bf16; 1 for f32): a ring row holds them in two halves of VS
+// entries, copied by two 1-D bulk copies (TMA).  The kernel is persistent and cooperative (one
+// CTA per SM) and runs k = floor(148 / Cc) groups of Cc = ceil(C / NH) CTAs: CTA (g, s) takes
+// core slice s of units g, g + k, ..., so a unit's items run concurrently on Cc SMs, which
+// exchange per-slice (max, sum) records through global memory (L2).
 //
-// Two passes per item; pass 2 needs the row normalisers, i.e. the records of all C
-// slices, so an item stays on chip from its arrival until the exchange completes
-// (several microseconds under full HBM load).  Two kinds of item keep it on chip:
+// Two passes per item; pass 2 needs the row normalisers, i.e. the records of all C slices,
+// so an item stays on chip from its arrival until the exchange completes (several
+// microseconds under full HBM load).  Two kinds of item keep it on chip:
 //   T items  pass 1 parks the exponentials e in TMEM (fp32) and releases the ring stage at
 //            once; pass 2 reads e back (tcgen05.ld) -- no recomputation.
 //   R items  pass 1 keeps the ring stage (bf16, half the bytes of e); pass 2 recomputes e
 //            from it (one more MUFU.EX2 per element) and releases the stage.
 // Of every pat_p items the first pat_t are T items (host-chosen).
 //
-// Exponent reference.  e = 2^((z - R) log2 e) needs no maximum: any R works while no
-// z - R exceeds ~88 (fp32 range).  The fast path takes R_l = the slice's first logit of row
-// l, read by every thread with one broadcast load, so all warps of the slice share it: no
-// max tree, no cross-lane max, and the per-warp factors of the exchange are all 1.  A
-// non-finite result (overflow, -inf or NaN inputs, a masked first entry) sends the warp to
-// the clamped slow path, whose reference is the warp maximum (records carry their warp's
-// reference, so the two mix freely).  Greedy mode (argmax needed) always takes the max path.
+// Exponent reference: the warp maximum of each row over the warp's region (the dominant
+// entries then have |z - m| small, so the fp32 exponent argument keeps full relative accuracy;
+// a fixed reference such as the first logit was measured to break the KL tolerance).
 //
-// Warp roles (7 service + 4 pass-2 + 8 pass-1 warps; low warp ids first):
-//   producer  TMA bulk copies (cp.async.bulk) of the L row slices into the S-stage ring.
-//   publisher folds the pass-1 warp records into the slice record and publishes it.
-//   fetchers  (items j = f mod NFETCH) poll the unit's L x C records, combine them into the
-//             row normalisers relative to this slice's references, and derive the pass-2
-//             factors.
-//   reducer   folds the pass-2 records into the slice residual R_s (probability units).
-//   pass 2    per-region residual sum max(e_l - rho e_{l-1}, 0) of every adjacent pair --
-//             this slice's share of DTV (Eq. 5) and of the residual CDF.
-//   pass 1    warp w owns the contiguous 512-entry region [512 w, 512 w + 512) of the slice
-//             (warps past the slice end idle): y = z - R with the mixed-precision
-//             add.f32.bf16 (no unpacking), e = 2^(y log2 e) on the MUFU, the sum of e and the
-//             KL numerator sum e_l (y_l - y_{l-1}) in packed fp32.
+// Warp roles (low warp ids first: the latency-critical ones; 28 warps, 72 registers):
+//   producer  (warp 0)  TMA bulk copies of the L row halves into the S-stage ring.
+//   publisher (warp 1)  folds the pass-1 warp records into one record per (row, tail slice)
+//                       and publishes it (exchange record first, then the tail's Partial).
+//   fetcher   (warp 2)  polls the unit's L x C records, combines them into the row
+//                       normalisers relative to this CTA's first slice, and derives the pass-2
+//                       factors of every (row, region).
+//   reducer   (warp 3)  folds the pass-2 records into the per-slice residuals R_s.
+//   pass 2    (8 warps) per-region residual sum max(e_l - rho e_{l-1}, 0) of every adjacent
+//                       pair -- this slice's share of DTV (Eq. 5) and of the residual CDF.
+//   pass 1    (2 x 8)   two groups take alternate items; warp r of a group owns the contiguous
+//                       1024-entry region r of the item (regions past a slice's end idle):
+//                       y = z - m with the mixed-precision add.f32.bf16 (no unpacking),
+//                       e = 2^(y log2 e) on the MUFU, the sum of e and the KL numerator
+//                       sum e_l (z_l - z_{l-1}) of the raw logit differences in packed fp32.
 #include "msd_common.cuh"
 #include "msd_internal.h"
 
@@ -1094,10 +1094,6 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     if (warp == W_PROD) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(c.taddr));
 }
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 
 template <typename Tin, int L, bool G>
 static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
@@ -1109,12 +1105,12 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     const size_t ctl = align_up(sizeof(Ctl<L>), 128);
     const size_t stage_bytes = (size_t)L * p.rs * ES;
     int S = (int)((SMEM_BUDGET - ctl - 256) / stage_bytes);
-    S = std::min(S, std::min(SMAX, env_int("MSD_STAGES", SMAX)));
+    S = std::min(S, std::min(SMAX, g_knobs.stages > 0 ? (int)g_knobs.stages : SMAX));
     if (S < 2) return cudaErrorInvalidConfiguration;
     p.stages = S;
     // item pattern: T items use the NT TMEM slots; R items keep their ring stage.  Of the S
     // stages ~4 are needed in flight for the TMA; the rest may hold R items.
-    int pt = env_int("MSD_PAT_T", NT), pr = env_int("MSD_PAT_R", -1);
+    int pt = g_knobs.pat_t >= 0 ? (int)g_knobs.pat_t : NT, pr = g_knobs.pat_r;
     if (pr < 0) pr = std::max(0, std::min(2, S - 3));
     if (pt < 1) pt = 1;
     p.pat_t = pt;
@@ -1139,29 +1135,6 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     const int64_t grid = kg * Cc;
     void* args[] = {&p};
     return cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(CORE_THREADS), args, smem, s);
-}
-
-// 0xF1 bytes: bf16 0xF1F1 and f32 0xF1F1F1F1 are both ~ -2.4e30, i.e. masked (-inf after the
-// -1e30 clamp) -- the fill of a row's last slice beyond the vocabulary
-__device__ __align__(128) unsigned char g_pad[VS * 4];
-
-cudaError_t core_pad(const void** out) {
-    static bool done[64] = {};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    void* ptr = nullptr;
-    e = cudaGetSymbolAddress(&ptr, g_pad);
-    if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64 && !done[dev]) {
-        e = cudaMemset(ptr, 0xF1, sizeof(g_pad));
-        if (e != cudaSuccess) return e;
-        e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) return e;
-        done[dev] = true;
-    }
-    *out = ptr;
-    return cudaSuccess;
 }
 
 cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s) {

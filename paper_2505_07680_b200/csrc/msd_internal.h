@@ -39,13 +39,11 @@ struct CoreParams {
     uint32_t* err;
     unsigned long long* trace;   // debug: 16 globaltimer stamps per item, or NULL
     int32_t dbg;                 // debug isolation mode (MSD_CORE_DBG): 0 = normal
-    const void* pad;             // >= VS * 4 bytes of 0xF1 (bf16 / f32 ~ -2.4e30, below the -1e30 clamp)
 };
 
-// the constant pad buffer of the current device (filled on first use)
-cudaError_t core_pad(const void** out);
-// exp of every bf16 value in float64 (65536 entries, filled on first use per device)
-cudaError_t exp_table(const double** out);
+// exp of every bf16 value in float64 (65536 entries), filled once per device by msd_init (or
+// lazily by the first verify call): `init` = 1 fills it on a private stream and waits for it
+cudaError_t exp_table(const double** out, int init);
 
 struct TailParams {
     LevelDesc lv;
@@ -105,6 +103,13 @@ struct RollbackParams {
     const int32_t* rollback;
     uint32_t* flags;
 };
+
+// Test / diagnostic overrides (msd_debug_set_knobs); the defaults are the release behaviour.
+struct DebugKnobs {
+    int32_t pat_t = -1, pat_r = -1, stages = -1, core_dbg = 0, exact_draws = 0;
+    double z_safe = 0.05;
+};
+extern DebugKnobs g_knobs;
 
 // Returns cudaSuccess or the launch error.  bf16 = 1 for bf16 logits, 0 for f32.
 cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s);

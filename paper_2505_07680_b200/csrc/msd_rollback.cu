@@ -23,11 +23,14 @@ __global__ void __launch_bounds__(RT) rollback_kernel(RollbackParams p) {
     if (tid == 0) s_total = 0;
     __syncthreads();
 
+    // a request is left untouched (ROLLBACK_OVF) when r is negative, exceeds its length, or its
+    // length claims more blocks than its block-table row holds (an inconsistent caller state)
+    const int64_t cap_tokens = (int64_t)kv.max_blocks * bs;
     // pass A: total number of blocks released by this model
     int32_t tot = 0;
     for (int b = tid; b < p.B; b += RT) {
         const int32_t old = kv.seq_len[b], rb = r[b];
-        if (rb < 0 || rb > old) continue;
+        if (rb < 0 || rb > old || old > cap_tokens) continue;
         const int32_t nw = old - rb;
         tot += (old + bs - 1) / bs - (nw + bs - 1) / bs;
     }
@@ -46,7 +49,7 @@ __global__ void __launch_bounds__(RT) rollback_kernel(RollbackParams p) {
         if (b < p.B) {
             old = kv.seq_len[b];
             const int32_t rb = r[b];
-            valid = rb >= 0 && rb <= old;
+            valid = rb >= 0 && rb <= old && old <= cap_tokens;
             if (valid) {
                 nw = old - rb;
                 n = (old + bs - 1) / bs - (nw + bs - 1) / bs;

@@ -1023,19 +1023,19 @@ __global__ void exp_table_kernel(double* tab) {
 }
 __device__ double g_exptab[65536];
 
-cudaError_t exp_table(const double** out) {
-    static bool done[64] = {};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
+cudaError_t exp_table(const double** out, int init) {
     void* ptr = nullptr;
-    e = cudaGetSymbolAddress(&ptr, g_exptab);
+    cudaError_t e = cudaGetSymbolAddress(&ptr, g_exptab);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64 && !done[dev]) {
-        exp_table_kernel<<<256, 256>>>(reinterpret_cast<double*>(ptr));
-        e = cudaDeviceSynchronize();
+    if (init) {
+        cudaStream_t st;
+        e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
         if (e != cudaSuccess) return e;
-        done[dev] = true;
+        exp_table_kernel<<<256, 256, 0, st>>>(reinterpret_cast<double*>(ptr));
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+        if (e != cudaSuccess) return e;
     }
     *out = reinterpret_cast<const double*>(ptr);
     return cudaSuccess;

@@ -48,13 +48,20 @@ def test_configs_match_oracle(name, kw):
     print(name, rep)
 
 
-@pytest.mark.parametrize("pat_t,pat_r", [(5, 0), (1, 6), (3, 2)])
-def test_item_patterns_agree(monkeypatch, pat_t, pat_r):
+@pytest.fixture
+def knobs():
+    """msd_debug_set_knobs overrides, restored to the release defaults afterwards."""
+    yield api.debug_knobs
+    api.debug_knobs()
+
+
+@pytest.mark.parametrize("pat_t,pat_r,stages", [(2, 0, -1), (1, 3, -1), (2, 2, -1), (2, 1, 3)])
+def test_item_patterns_agree(knobs, pat_t, pat_r, stages):
     """T items (exponentials parked in TMEM) and R items (ring stage kept, pass 2 recomputes)
-    must give the same accept / emit decisions and divergences as the oracle, in any mix."""
+    must give the same accept / emit decisions and divergences as the oracle, in any mix and
+    ring depth."""
     inp = _gauss("llama3", B=24, V=30000)
-    monkeypatch.setenv("MSD_PAT_T", str(pat_t))
-    monkeypatch.setenv("MSD_PAT_R", str(pat_r))
+    knobs(pat_t=pat_t, pat_r=pat_r, stages=stages)
     o = _run(inp)
     assert_parity(o, run_oracle(inp))
 
@@ -205,10 +212,10 @@ def test_verify_level_composes_to_chain_verify():
     assert np.array_equal(last["out_len"], o["commit_len"])
 
 
-def test_exact_draw_mode_agrees_with_fast_path(monkeypatch):
+def test_exact_draw_mode_agrees_with_fast_path(knobs):
     inp = _gauss("qwen25", B=10, V=60000)
     fast = {k: v.clone() for k, v in _run(inp).items()}
-    monkeypatch.setenv("MSD_EXACT_DRAWS", "1")
+    knobs(exact_draws=True)
     exact = _run(inp)
     ref = run_oracle(inp)
     assert_parity(exact, ref)
@@ -235,6 +242,9 @@ def test_kv_rollback_matches_oracle():
     r = torch.stack([torch.minimum(torch.randint(0, 40, (B,), generator=g), kv[i]["seq_len"].cpu())
                      for i in range(nm)]).to(torch.int32)
     r[1, 7] = 10_000                                     # overflow -> flagged, untouched
+    mb = kv[0]["block_table"].shape[1]
+    kv[0]["seq_len"][11] = mb * 16 + 5                   # beyond its block-table row (R22)
+    r[0, 11] = 3
     masks = []
     for i in range(nm):
         cm = torch.zeros((B, 760), dtype=torch.uint8)
@@ -256,7 +266,7 @@ def test_kv_rollback_matches_oracle():
         assert int(kv[i]["free_count"][0]) == o["free_count"]
         assert np.array_equal(kv[i]["free_ids"].cpu().numpy(), o["free_ids"])
         assert np.array_equal(kv[i]["cache_mask"].cpu().numpy(), o["cache_mask"])
-    assert fl[7] & api.FLAG["ROLLBACK_OVF"]
+    assert fl[7] & api.FLAG["ROLLBACK_OVF"] and fl[11] & api.FLAG["ROLLBACK_OVF"]
 
 
 def test_kv_rollback_freelist_overflow():

@@ -131,3 +131,14 @@ def test_paged_rollback_overflow_and_freelist_flags():
     o = O.rollback_paged(np.array([40], np.int32), np.array([[0, 1, 2]], np.int32), 16, free, 0,
                          np.array([39], np.int32))
     assert o["flags"][0] & 16 and o["seq_len"][0] == 1 and (o["block_table"] == [[0, 1, 2]]).all()
+
+
+def test_paged_rollback_rejects_a_length_beyond_the_block_table_row():
+    # DESIGN.md R22: a sequence longer than its block-table row can hold is an inconsistent
+    # caller state; the request is left untouched and flagged, the others proceed
+    bt = np.arange(2 * 3, dtype=np.int32).reshape(2, 3)          # 3 blocks of 4 tokens per row
+    o = O.rollback_paged(np.array([13, 9]), bt, 4, np.full(8, -1, np.int32), 0, np.array([2, 5]))
+    assert o["seq_len"].tolist() == [13, 4] and o["flags"][0] != 0 and o["flags"][1] == 0
+    assert o["block_table"][0].tolist() == [0, 1, 2]                   # untouched
+    assert o["block_table"][1].tolist() == [3, -1, -1] and o["free_count"] == 2
+    assert o["free_ids"][:2].tolist() == [4, 5]

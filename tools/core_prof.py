@@ -2,14 +2,15 @@
 
 Prints, per role, the average SM cycles per item spent in each phase (summed over warps of
 the role, divided by the items those warps processed), plus the kernel time.
-usage: MSD_LIB=libmsd_prof.so python tools/core_prof.py [config]   (env MSD_PAT_T / MSD_PAT_R /
-MSD_STAGES select the item pattern and ring depth)"""
+usage: MSD_LIB=libmsd_prof.so python tools/core_prof.py [config] [pat_t,pat_r,stages]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2505_07680_b200 import api, synth
 name = sys.argv[1] if len(sys.argv) > 1 else "llama3"
 c = synth.CONFIGS[name]
+pat = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "-1,-1,-1").split(",")]
+api.debug_knobs(pat_t=pat[0], pat_r=pat[1], stages=pat[2])
 inp = synth.gauss_chain(c["B"], c["V"], c["K"], c["L"], c["sigmas"], s=c["s"], seed=c["seed"], device="cuda", dtype=c["dtype"])
 cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"])
 lib = api.lib(); lib.msd_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
@@ -28,7 +29,7 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 e0.record(); cv(); e1.record(); torch.cuda.synchronize()
 lib.msd_debug_set_trace(None, 0)
 a = buf[:96].view(6, 16).cpu().double()
-print(f"{name}: step (core+tail, profiled) {e0.elapsed_time(e1):.3f} ms  PAT_T={os.environ.get('MSD_PAT_T','dflt')} PAT_R={os.environ.get('MSD_PAT_R','dflt')} STAGES={os.environ.get('MSD_STAGES','dflt')}")
+print(f"{name}: step (core+tail, profiled) {e0.elapsed_time(e1):.3f} ms  pattern {pat}")
 for r, (rn, ph) in roles.items():
     n = a[r, 15].item()
     if n == 0:
