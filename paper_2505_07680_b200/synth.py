@@ -153,3 +153,17 @@ def paged_kv(B: int, n_models: int, *, seed: int, block_size: int = 16, min_len:
                         free_count=torch.tensor([nfree], dtype=torch.int32, device=device),
                         block_size=block_size, max_blocks=max_blocks))
     return out
+
+
+def draft_tokens(z: torch.Tensor, K: int, V: int, *, seed: int, req0: int = 0, salt: int = 0) -> torch.Tensor:
+    """Draft tokens x[b,i] ~ softmax(z[b,i,:V]) for i < K by the Gumbel-max trick, one generator
+    per request (seed, global request id, salt) -- the drafter of a sub-chain that does not start
+    at the pool's first model (adaptive sweep)."""
+    B = z.shape[0]
+    out = torch.empty((B, K), dtype=torch.int32, device=z.device)
+    gen = torch.Generator(device=z.device)
+    for b in range(B):
+        gen.manual_seed(_mix(seed, req0 + b, salt=100 + salt))
+        g = torch.rand((K, V), generator=gen, device=z.device).clamp_(min=1e-30)
+        out[b] = (z[b, :K, :V].float() - torch.log(-torch.log(g))).argmax(dim=1).to(torch.int32)
+    return out
