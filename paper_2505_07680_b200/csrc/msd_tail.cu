@@ -37,6 +37,10 @@ constexpr double TIE_EPS = 1e-6;
 // from the chosen slice's and token's boundaries; the fp32-derived masses drift by ~3e-8 / Z
 // (R4), far inside the margin.  Otherwise the exact path decides.
 constexpr double DRAW_MARGIN_REL = 2e-5, DRAW_MARGIN_ABS = 0.0;
+// u Z this close (relative to Z) to a slice boundary of the fp32-derived slice prefix: the slice
+// itself may be the wrong one (prefix error ~1e-7 Z), so the exact path re-selects it from
+// float64 slice masses
+constexpr double SLICE_MARGIN_REL = 1e-6;
 
 struct TailShared {
     RowStat row[MAXC][MAXL];      // row statistics of draft positions i < K (from the core partials)
@@ -56,7 +60,7 @@ struct TailShared {
     uint32_t flags;
     int32_t near;
     int32_t exact;
-    double sel_before;
+    double sel_before, sel_after;
     int32_t sel_slice;
     float zpre[MAXL][MAXC];       // z_l[b, i, x_i]: the draft token's logit in every row i < K
     const double* exptab;         // exp of every bf16 value (float64), or NULL
@@ -545,7 +549,7 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
         const double target = u * Z;
         double base = 0.0;
         int sel = -1, lastpos = -1;
-        double before = 0.0;
+        double before = 0.0, after = 0.0;
         for (int s0 = 0; s0 < C; s0 += 32) {
             const double ws = (s0 + lane < C) ? sh.w[s0 + lane] : 0.0;
             double incl = ws;
@@ -561,6 +565,7 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
                 const int f = __ffs((int)hit) - 1;
                 sel = s0 + f;
                 before = base + __shfl_sync(0xffffffffu, incl - ws, f);
+                after = base + __shfl_sync(0xffffffffu, incl, f);
             }
             base += __shfl_sync(0xffffffffu, incl, 31);
         }
@@ -568,12 +573,15 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
         if (lane == 0) {
             sh.sel_slice = sel;
             sh.sel_before = before;
+            sh.sel_after = after;
         }
     }
     __syncthreads();
     const int sel = sh.sel_slice;
-    const double before = sh.sel_before;
+    const double before = sh.sel_before, after = sh.sel_after;
     __syncthreads();
+    if (!exact && sel >= 0 && (u * Z - before < SLICE_MARGIN_REL * Z || after - u * Z < SLICE_MARGIN_REL * Z))
+        return -1;      // next to a slice boundary: the caller takes the exact path
     if (sel < 0) {  // u*Z beyond the total (rounding): clamp to the last positive entry
         *tie = true;
         return last_positive<Tin>(resid, ra, rb, A, B, V, -1 - sel, vse, sh);
