@@ -378,6 +378,13 @@ __device__ __forceinline__ void load16(const Tin* row, int64_t e0, int64_t Vend,
 // exp(z - S) in float64.  For bf16 logits (every z is a bf16 value) it is tab[bits(z)] * e^-S
 // with tab[h] = exp(bf16 h) (msd_api: exp_table), one lookup and one multiply instead of a
 // float64 exp; outside the table's range (|z| >= 700, |S| >= 700) the FMA-pipe dexp_neg.
+#ifndef MSD_EXACT_U
+#define MSD_EXACT_U 1
+#endif
+// out of line: the rare fallback must not be unrolled into the table loops (inlined, its copies
+// made the exact draw instruction-cache bound: 'no_inst' stalls at the table gathers)
+__device__ __noinline__ double dexp_neg_cold(double x) { return dexp_neg(x); }
+
 struct ExpShift {
     const double* tab;   // NULL: no table (f32 logits)
     double S, eS;
@@ -391,7 +398,7 @@ struct ExpShift {
             const double t = __ldg(tab + (__float_as_uint(z) >> 16));
             if (t == t) return t * eS;      // NaN entry: outside the table's range
         }
-        return dexp_neg((double)z - S);     // z <= max <= S: argument <= 0
+        return dexp_neg_cold((double)z - S);     // z <= max <= S: argument <= 0
     }
 };
 
@@ -402,7 +409,7 @@ __device__ __forceinline__ void exp_shift_batch(const ExpShift& es, const float*
 #pragma unroll
     for (int k = 0; k < N; ++k) out[k] = __ldg(es.tab + (__float_as_uint(z[k]) >> 16));
 #pragma unroll
-    for (int k = 0; k < N; ++k) out[k] = (out[k] == out[k]) ? out[k] * es.eS : dexp_neg((double)z[k] - es.S);
+    for (int k = 0; k < N; ++k) out[k] = (out[k] == out[k]) ? out[k] * es.eS : dexp_neg_cold((double)z[k] - es.S);
 }
 
 __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, double B) {
@@ -611,7 +618,8 @@ __device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin*
   eMb.init(tab, Br.M);
   double sa = 0.0, sb = 0.0;
   {
-      constexpr int U = 4;
+      constexpr int U = MSD_EXACT_U;   // compact loop (a 4x unrolled one was slower: 370 vs 240 us)
+#pragma unroll 1
       for (int64_t e0 = (int64_t)threadIdx.x * VEC; e0 < V; e0 += (int64_t)U * T * VEC) {
           float xa[U][VEC], xb[U][VEC];
 #pragma unroll
@@ -659,7 +667,8 @@ __device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin*
     for (int s = warp; s < C; s += NWARP) {
         const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
         double acc = 0.0;
-        constexpr int U = 4;    // vector pairs in flight per lane (HBM round trips dominate)
+        constexpr int U = MSD_EXACT_U;
+#pragma unroll 1
         for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
             float xa[U][VEC], xb[U][VEC];
 #pragma unroll
