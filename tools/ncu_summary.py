@@ -66,7 +66,7 @@ def launches(src, out):
         n = r[h.index("Kernel Name")]
         v = float(r[h.index("Metric Value")].replace(",", ""))
         agg.setdefault(n, []).append(v)
-    ours = lambda n: "msd::" in n or any(k in n for k in ("core_kernel", "tail_kernel", "rollback_kernel", "exp_table_kernel"))
+    ours = lambda n: "msd::" in n or any(k in n for k in ("core_kernel", "tail_kernel", "rollback_kernel", "exp_table_kernel", "pool_kernel", "draft_kernel"))
     tot = sum(sum(v) for n, v in agg.items() if ours(n))
     with open(out, "w", newline="") as f:
         w = csv.writer(f)
