@@ -91,6 +91,7 @@ struct Ctl {
     uint64_t rowf_full[NQ], rowf_empty[NQ];
     uint64_t tm_full[NTMAX], tm_empty[NTMAX];  // TMEM item slots: pass-1 warps -> pass-2 warps
     uint64_t pub[NQ];                       // this CTA's slice record of item j is published
+    uint32_t p1cnt[R1];                     // pass-1 warps done with the item of a record slot
     uint32_t taddr;
     float wmx[NQ][L][NCW];                  // per-warp max of each row, per item
     uint32_t clampw[NQ];                    // bit w: pass-1 warp w took the clamped path
@@ -130,6 +131,9 @@ __device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
           "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
         : "r"(ta));
 }
+#ifndef MSD_INLINE_PUB
+#define MSD_INLINE_PUB 0               // 1: the last pass-1 warp of an item publishes its records (measured slower: 1.06 vs 1.00 ms)
+#endif
 #ifndef MSD_SPIN_SERVICE
 #define MSD_SPIN_SERVICE 1
 #endif
@@ -464,6 +468,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid < NQ) c.clampw[tid] = 0u;
+    if (tid < R1) c.p1cnt[tid] = 0u;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -482,6 +487,73 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     };
     // TMEM column base of region w (lane quadrant w & 3, column block w >> 2)
     auto tcol = [&](int w) { return c.taddr + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((w >> 2) * TCOLS); };
+
+    // Publisher (one full warp; run by the last pass-1 warp of the item, or the publisher warp):
+    // lane = 8 l + w: row l, region w (L <= 4).  Each lane sums its region's sub-records, scales
+    // them by 2^((m_w - m_s) log2 e) relative to the tail slice's maximum m_s (1 when the region
+    // holds the maximum) and the HREG lanes of each half reduce with 2 shuffle levels: one record
+    // per (row, tail slice NH s + w / HREG).
+    static_assert(NCW == 8 && HREG == 4 && L * NCW <= 32, "publisher lane layout");
+    auto publish = [&](int j) {
+        const int l = lane >> 3, w = lane & 7;
+        const bool inrow = l < L;
+        const bool act = inrow && ((amask >> w) & 1u);
+        const int tslice = NH * s + w / HREG;   // this lane's tail slice
+        int64_t u, b, i;
+        item(j, u, b, i);
+        const int k = j & (NQ - 1);
+        const int r1 = j & (R1 - 1);
+        float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
+        int aw = 0x7fffffff;
+        if (act) {
+            const float4 s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
+            const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][w][0]);
+            Sw = (s4.x + s4.y) + (s4.z + s4.w);
+            Kw = (k4.x + k4.y) + (k4.z + k4.w);
+            wm = c.wmx[k][l][w];
+            if (GREEDY) aw = c.r1A[r1][l][w];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            c.p1cnt[r1] = 0u;               // the next item of this record slot counts from 0
+            mbar_arrive(&c.r1_empty[r1]);
+        }
+        // tail-slice maximum of the row (NaN-propagating) over the half's HREG lanes
+        float msl = wm;
+#pragma unroll
+        for (int o = HREG / 2; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
+        float f = wm == msl ? 1.f : ex2f((wm - msl) * LOG2E);
+        if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
+        // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
+        float Sx = Sw * f, Kx = (l > 0 && f != 0.f) ? f * Kw : 0.f;
+        int ax = (wm == msl) ? aw : 0x7fffffff;
+#pragma unroll
+        for (int o = HREG / 2; o > 0; o >>= 1) {
+            Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
+            Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
+            if (GREEDY) ax = min(ax, __shfl_xor_sync(0xffffffffu, ax, o));
+        }
+        if (lane == 0) stamp(j, 9);
+        // lanes 8 l and 8 l + HREG publish row l's records of the two tail slices: first the
+        // self-validating exchange record (the other slices wait for it; sum != 0: the slice
+        // maximum's entry has e = 1 in the sum), then the Partial for the tail
+        if (inrow && (w % HREG) == 0 && w / HREG < NH && tslice < C) {
+            const size_t idx = ((size_t)u * L + l) * C + tslice;
+            st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
+                           ((unsigned long long)__float_as_uint(Sx) << 32) | __float_as_uint(msl));
+            Partial pr;
+            pr.m = msl;
+            pr.amax = GREEDY ? ax : 0;
+            pr.S = f2d_alu(Sx);
+            pr.Kl = f2d_alu(Kx);
+            p.partials[idx] = pr;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            stamp(j, 5);
+            mbar_arrive(&c.pub[k]);
+        }
+    };
 
     const bool p1only = (p.dbg & 1) != 0;   // debug: pass 1 + TMA ring only (results invalid)
     if (p1only && warp != W_PROD && warp < W_P1) {
@@ -676,9 +748,24 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     atomicMax(p.trace + ((int64_t)(grp + j * kgrp) * Cc + sfix) * 16 + 7, (unsigned long long)globaltimer());
 #endif
                 if (lane == 0 && !p1only) {
-                    mbar_arrive(&c.r1_full[r1]);
+                    if (!MSD_INLINE_PUB) mbar_arrive(&c.r1_full[r1]);
                     if (isT) mbar_arrive(&c.tm_full[q]);
                 }
+#if MSD_INLINE_PUB
+                if (!p1only) {
+                    // the last pass-1 warp of the item publishes its records at once (no wake-up
+                    // of a publisher warp): fence + counter, like a last-block reduction
+                    uint32_t last = 0;
+                    if (lane == 0) {
+                        __threadfence_block();
+                        last = atomicAdd(&c.p1cnt[r1], 1u) == (uint32_t)(nact - 1) ? 1u : 0u;
+                    }
+                    if (__shfl_sync(0xffffffffu, last, 0)) {
+                        __threadfence_block();
+                        publish(j);
+                    }
+                }
+#endif
                 PROF(5)
                 PROF_ITEM
                 for (int x = 0; x < NG1; ++x) cu.next(S, PP, PT, NT);
@@ -854,73 +941,17 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // scales them by 2^((m_w - m_s) log2 e) relative to the tail slice's maximum m_s (1 when
         // the region holds the maximum) and the HREG lanes of each half reduce with 2 shuffle
         // levels: one record per (row, tail slice NH s + w / HREG).
-        static_assert(NCW == 8 && HREG == 4 && L * NCW <= 32, "publisher lane layout");
         PROF_DECL
-        const int l = lane >> 3, w = lane & 7;
-        const bool inrow = l < L;
-        const bool act = inrow && ((amask >> w) & 1u);
-        const int tslice = NH * s + w / HREG;   // this lane's tail slice
+#if !MSD_INLINE_PUB
         for (int j = 0; j < n_my; ++j) {
-            int64_t u, b, i;
-            item(j, u, b, i);
-            const int k = j & (NQ - 1);
-            const int r1 = j & (R1 - 1);
-            mbar_wait_lat(&c.r1_full[r1], (uint32_t)((j / R1) & 1));
+            mbar_wait_lat(&c.r1_full[j & (R1 - 1)], (uint32_t)((j / R1) & 1));
             if (lane == 0) stamp(j, 8);
             PROF(0)
-            float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
-            int aw = 0x7fffffff;
-            if (act) {
-                const float4 s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
-                const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][w][0]);
-                Sw = (s4.x + s4.y) + (s4.z + s4.w);
-                Kw = (k4.x + k4.y) + (k4.z + k4.w);
-                wm = c.wmx[k][l][w];
-                if (GREEDY) aw = c.r1A[r1][l][w];
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c.r1_empty[r1]);
-            PROF(2)
-            // tail-slice maximum of the row (NaN-propagating) over the half's HREG lanes
-            float msl = wm;
-#pragma unroll
-            for (int o = HREG / 2; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
-            float f = wm == msl ? 1.f : ex2f((wm - msl) * LOG2E);
-            if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
-            // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
-            float Sx = Sw * f, Kx = (l > 0 && f != 0.f) ? f * Kw : 0.f;
-            int ax = (wm == msl) ? aw : 0x7fffffff;
-            PROF(3)
-#pragma unroll
-            for (int o = HREG / 2; o > 0; o >>= 1) {
-                Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
-                Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
-                if (GREEDY) ax = min(ax, __shfl_xor_sync(0xffffffffu, ax, o));
-            }
-            PROF(4)
-            if (lane == 0) stamp(j, 9);
-            // lanes 8 l and 8 l + HREG publish row l's records of the two tail slices: first the
-            // self-validating exchange record (the other slices wait for it; sum != 0: the slice
-            // maximum's entry has e = 1 in the sum), then the Partial for the tail
-            if (inrow && (w % HREG) == 0 && w / HREG < NH && tslice < C) {
-                const size_t idx = ((size_t)u * L + l) * C + tslice;
-                st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
-                               ((unsigned long long)__float_as_uint(Sx) << 32) | __float_as_uint(msl));
-                Partial pr;
-                pr.m = msl;
-                pr.amax = GREEDY ? ax : 0;
-                pr.S = f2d_alu(Sx);
-                pr.Kl = f2d_alu(Kx);
-                p.partials[idx] = pr;
-            }
-            __syncwarp();
-            if (lane == 0) {
-                stamp(j, 5);
-                mbar_arrive(&c.pub[k]);
-            }
+            publish(j);
             PROF(1)
             PROF_ITEM
         }
+#endif
         PROF_FLUSH(2)
     } else if (warp >= W_FETCH0 && warp < W_FETCH0 + NFETCH) {
         // ================================================================ fetchers (pass-2 factors)
