@@ -191,6 +191,7 @@ msd_status run_engine(const Engine& E) {
     cp.ready = reinterpret_cast<uint32_t*>(ws + w.ready);
     cp.flags = E.flags;
     cp.err = reinterpret_cast<uint32_t*>(ws + w.hdr);
+    cp.board = reinterpret_cast<JobBoard*>(ws + w.board);
     cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
     cp.dbg = g_knobs.core_dbg;
 
@@ -207,6 +208,7 @@ msd_status run_engine(const Engine& E) {
     tp.pos_dtv = E.pos_dtv; tp.pos_kl = E.pos_kl; tp.stats = E.stats; tp.flags = E.flags;
     tp.partials = cp.partials; tp.partms = cp.partms; tp.resid = cp.resid;
     tp.cnt = cp.cnt;
+    tp.board = cp.board;
     tp.z_safe = g_knobs.z_safe;                  // exact draws below this residual mass (R4)
     tp.exact_all = g_knobs.exact_draws;
     {

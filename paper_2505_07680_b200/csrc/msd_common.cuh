@@ -71,9 +71,33 @@ __host__ __device__ inline SliceGeom slice_geometry(int64_t V) {
     return g;
 }
 
+// Exact-draw work sharing inside the tail kernel (msd_tail.cu): a request that needs an exact
+// float64 draw posts a job; CTAs that finished their own request claim its chunks (normaliser
+// chunks of the row pair, then slice masses).  Reset by the core kernel before every tail.
+constexpr int EXJ_MAX = 32;        // concurrent jobs (more: the requester works alone)
+constexpr int EXJ_NCH = 16;        // normaliser chunks per job
+constexpr int EXJ_SPC = 4;         // slices per slice-mass chunk
+constexpr int EXJ_MAXS = 128;      // slices per job (= the tail's MAXSLICES)
+struct ExactJob {
+    const void* ra;
+    const void* rb;
+    double Ma, Mb, A, B;
+    int64_t V;
+    int32_t resid, C, vse, chunk;
+    uint32_t phase;                // 0 free / being filled, 1 normalisers, 2 slice masses, 3 done
+    uint32_t next1, done1, next2, done2;
+    uint32_t pad[5];
+};
+struct JobBoard {
+    uint32_t alloc, started, finished, pad0;
+    ExactJob job[EXJ_MAX];
+    double part1[EXJ_MAX][EXJ_NCH][2];
+    double part2[EXJ_MAX][EXJ_MAXS];
+};
+
 // Workspace layout (bytes), shared by host and device code.
 struct WsLayout {
-    size_t hdr, cnt, ready, partials, partms, rowstat, kl, resid, total;
+    size_t hdr, cnt, ready, partials, partms, rowstat, kl, resid, board, total;
     int32_t U, C, L;
 };
 
@@ -95,6 +119,7 @@ __host__ __device__ inline WsLayout ws_layout(int32_t L, int32_t B, int32_t K, i
     w.rowstat = off;  off = align_up(off + sizeof(RowStat) * (size_t)w.U * L, 256);
     w.kl = off;       off = align_up(off + sizeof(double) * (size_t)w.U * (L - 1), 256);
     w.resid = off;    off = align_up(off + sizeof(double) * (size_t)w.U * (L - 1) * w.C, 256);
+    w.board = off;    off = align_up(off + sizeof(JobBoard), 256);
     w.total = off;
     return w;
 }

@@ -77,7 +77,9 @@ constexpr int NTMAX = 8;               // TMEM item slots (upper bound)
 constexpr int FBUF = 192;              // records per fetcher staging buffer (L * C <= 192)
 constexpr int SMEM_BUDGET = 227 * 1024;
 constexpr int R1 = 4, R2 = 4;          // pass-1 / pass-2 record rings (powers of two)
-constexpr int NSUB = 4;                // per-warp records after a 3-step shuffle fold (lanes 0..3)
+constexpr int NSUB = 4;                // per-warp pass-2 records after a 3-step shuffle fold (lanes 0..3)
+constexpr int NSUB1 = 4;               // per-warp pass-1 records after a 3-step shuffle fold (lanes
+                                       // 0..3): the publisher sums them in float64 (KL / LSE precision)
 static_assert(NCW == 2 * HREG, "two halves of HREG regions");
 
 struct WF {                // pass-2 factors of one (row, warp) of the current slice
@@ -95,8 +97,8 @@ struct Ctl {
     uint32_t taddr;
     float wmx[NQ][L][NCW];                  // per-warp max of each row, per item
     uint32_t clampw[NQ];                    // bit w: pass-1 warp w took the clamped path
-    alignas(16) float r1S[R1][L][NCW][NSUB];   // pass-1 partial sums
-    alignas(16) float r1K[R1][L][NCW][NSUB];   // pass-1 KL numerators (relative to the warp shift)
+    alignas(16) float r1S[R1][L][NCW][NSUB1];  // pass-1 partial sums
+    alignas(16) float r1K[R1][L][NCW][NSUB1];  // pass-1 KL numerators sum e (z_l - z_{l-1})
     int r1A[R1][L][NCW];                    // greedy: first argmax index per warp
     WF rowf[NQ][L][NCW];
     float r2R[R2][L][NCW2][NSUB];           // pass-2 residual partials (probability units)
@@ -131,6 +133,9 @@ __device__ __forceinline__ void tm_ld16(uint32_t ta, float* v) {
           "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
         : "r"(ta));
 }
+#ifndef MSD_PUB_LATE
+#define MSD_PUB_LATE 1                 // this CTA's fetcher starts polling after the Partials too (0: earlier polling, measured 3 % slower)
+#endif
 #ifndef MSD_INLINE_PUB
 #define MSD_INLINE_PUB 0               // 1: the last pass-1 warp of an item publishes its records (measured slower: 1.06 vs 1.00 ms)
 #endif
@@ -468,6 +473,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid < NQ) c.clampw[tid] = 0u;
+    if (blockIdx.x == 0 && p.board) {       // the tail's exact-draw job board, for this call
+        for (int t = tid; t < 4 + EXJ_MAX * (int)(sizeof(ExactJob) / 4); t += blockDim.x)
+            reinterpret_cast<uint32_t*>(p.board)[t] = 0u;
+    }
     if (tid < R1) c.p1cnt[tid] = 0u;
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -504,9 +513,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         const int k = j & (NQ - 1);
         const int r1 = j & (R1 - 1);
         float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
         int aw = 0x7fffffff;
         if (act) {
-            const float4 s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
+            s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
             const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][w][0]);
             Sw = (s4.x + s4.y) + (s4.z + s4.w);
             Kw = (k4.x + k4.y) + (k4.z + k4.w);
@@ -530,29 +540,49 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) {
             Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
-            Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
             if (GREEDY) ax = min(ax, __shfl_xor_sync(0xffffffffu, ax, o));
         }
         if (lane == 0) stamp(j, 9);
-        // lanes 8 l and 8 l + HREG publish row l's records of the two tail slices: first the
-        // self-validating exchange record (the other slices wait for it; sum != 0: the slice
-        // maximum's entry has e = 1 in the sum), then the Partial for the tail
-        if (inrow && (w % HREG) == 0 && w / HREG < NH && tslice < C) {
-            const size_t idx = ((size_t)u * L + l) * C + tslice;
+        // lanes 8 l and 8 l + HREG publish row l's exchange records of the two tail slices first:
+        // the other slices wait for them (self-validating: sum != 0, the slice maximum's entry
+        // has e = 1 in the sum); this CTA's fetcher may start polling
+        const bool pub_lane = inrow && (w % HREG) == 0 && w / HREG < NH && tslice < C;
+        const size_t idx = ((size_t)u * L + l) * C + tslice;
+        if (pub_lane)
             st_relaxed_u64(reinterpret_cast<unsigned long long*>(p.partms) + idx,
                            ((unsigned long long)__float_as_uint(Sx) << 32) | __float_as_uint(msl));
-            Partial pr;
-            pr.m = msl;
-            pr.amax = GREEDY ? ax : 0;
-            pr.S = f2d_alu(Sx);
-            pr.Kl = f2d_alu(Kx);
-            p.partials[idx] = pr;
-        }
+#if !MSD_PUB_LATE
         __syncwarp();
         if (lane == 0) {
             stamp(j, 5);
             mbar_arrive(&c.pub[k]);
         }
+#endif
+        // then the tail's Partial, off the exchange's critical path: the slice sum again in
+        // float64 from the sub-records (the row normalisers' precision decides the KL and
+        // acceptance errors of the tail), the KL numerator in fp32
+        // (hardware float -> double conversions: off the latency path, few instructions)
+        double Sd = (((double)s4.x + (double)s4.y) + ((double)s4.z + (double)s4.w)) * (double)f;
+#pragma unroll
+        for (int o = HREG / 2; o > 0; o >>= 1) {
+            Sd += __shfl_xor_sync(0xffffffffu, Sd, o);
+            Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
+        }
+        if (pub_lane) {
+            Partial pr;
+            pr.m = msl;
+            pr.amax = GREEDY ? ax : 0;
+            pr.S = Sd;
+            pr.Kl = (double)Kx;
+            p.partials[idx] = pr;
+        }
+#if MSD_PUB_LATE
+        __syncwarp();
+        if (lane == 0) {
+            stamp(j, 5);
+            mbar_arrive(&c.pub[k]);
+        }
+#endif
     };
 
     const bool p1only = (p.dbg & 1) != 0;   // debug: pass 1 + TMA ring only (results invalid)
@@ -725,7 +755,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     else atomicOr(&c.clampw[k], bit);
                 }
                 PROF(3)
-                if (lane < NSUB) {
+                if (lane < NSUB1) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
                         c.r1S[r1][l][rg][lane] = Sv[l];

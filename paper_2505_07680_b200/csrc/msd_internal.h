@@ -11,6 +11,7 @@ namespace msd {
 
 struct Partial;
 struct RowStat;
+struct JobBoard;
 
 struct LevelDesc {
     const void* ptr[4];
@@ -37,6 +38,7 @@ struct CoreParams {
     uint32_t* ready;
     uint32_t* flags;
     uint32_t* err;
+    JobBoard* board;             // reset by CTA 0 before the roles start (the tail's exact-draw jobs)
     unsigned long long* trace;   // debug: 16 globaltimer stamps per item, or NULL
     int32_t dbg;                 // debug isolation mode (MSD_CORE_DBG): 0 = normal
 };
@@ -73,6 +75,7 @@ struct TailParams {
     int32_t exact_all;
     int32_t prefetch;   // set by launch_tail: partials + residuals of a request fit in shared memory
     const double* exptab;   // exp of every bf16 value (exact-draw path), from exp_table()
+    JobBoard* board;        // exact-draw work sharing (reset by the core kernel)
 };
 
 struct PoolParams {          // SimScore bootstrap (msd_pool.cu)

@@ -62,6 +62,7 @@ struct TailShared {
     int32_t exact;
     double sel_before, sel_after;
     int32_t sel_slice;
+    int32_t ex_job, ex_ok, ex_go, ex_pick, ex_phase, ex_chunk;   // exact-draw job board scratch
     float zpre[MAXL][MAXC];       // z_l[b, i, x_i]: the draft token's logit in every row i < K
     const double* exptab;         // exp of every bf16 value (float64), or NULL
 };
@@ -596,123 +597,241 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
     return scan_slice<Tin>(resid, ra, rb, A, B, V, sel, vse, before, u * Z, Z, u, sh, tie, exact);
 }
 
-// Exact float64 draw over the whole row (pair): exact normalisers, exact slice masses (one
-// warp per slice, fixed order), exact scan.  Residual mass < 1e-12 -> draw from p.
+// ------------------------------------------------------------------ exact draws
+// Exact float64 draw over the whole row (pair): exact normalisers, exact slice masses, exact
+// scan.  Residual mass < 1e-12 -> draw from p.  The two full-row passes are cut into
+// chunks (EXJ_NCH normaliser chunks, then one chunk per slice), each summed by one whole CTA
+// in a fixed order and combined in chunk order, so the result does not depend on which CTA
+// computed a chunk: the requesting CTA posts the job on the board and CTAs that finished
+// their own request help (exact_help); with no helper (or a full board) it does all chunks.
+
+// float64 sum of exp(z - M) over [e0, e1) of one row (and of the second row) -- whole CTA,
+// result valid in every thread (fixed order: strided per thread, then block_sum_d)
 template <typename Tin>
-__device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const RowStat& Ar,
-                              const RowStat& Br, int64_t V, int C, int vse, double u, TailShared& sh,
-                              bool* tie, bool* small) {
-  constexpr int VEC = Elem<Tin>::VEC;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef MSD_PROF
-  if (threadIdx.x == 0) g_tail_req[blockIdx.x][11] += (unsigned long long)clock64();
-#endif
-  // both rows into L2 up front: the normaliser pass then has every line in flight, and the
-  // slice-mass pass and the rescan below re-read them from L2
-  prefetch_row_l2(ra, V);
-  if (resid) prefetch_row_l2(rb, V);
-  // exact normalisers: every thread a strided set of whole vectors, 4 in flight
-  const double* tab = sizeof(Tin) == 2 ? sh.exptab : nullptr;
-  ExpShift eMa, eMb;
-  eMa.init(tab, Ar.M);
-  eMb.init(tab, Br.M);
-  double sa = 0.0, sb = 0.0;
-  {
-      constexpr int U = MSD_EXACT_U;   // compact loop (a 4x unrolled one was slower: 370 vs 240 us)
+__device__ void exact_norm_chunk(const Tin* ra, const Tin* rb, bool resid, int64_t e0, int64_t e1, double Ma,
+                                 double Mb, const double* tab, TailShared& sh, double* sa_out, double* sb_out) {
+    constexpr int VEC = Elem<Tin>::VEC;
+    ExpShift eMa, eMb;
+    eMa.init(tab, Ma);
+    eMb.init(tab, Mb);
+    double sa = 0.0, sb = 0.0;
 #pragma unroll 1
-      for (int64_t e0 = (int64_t)threadIdx.x * VEC; e0 < V; e0 += (int64_t)U * T * VEC) {
-          float xa[U][VEC], xb[U][VEC];
+    for (int64_t e = e0 + (int64_t)threadIdx.x * VEC; e < e1; e += (int64_t)T * VEC) {
+        float xa[VEC], xb[VEC];
+        load_vec<Tin>(ra, e, e1, xa);
+        if (resid) load_vec<Tin>(rb, e, e1, xb);
+        if (eMa.tab && (!resid || eMb.tab)) {
+            double ga[VEC], gb[VEC];
+            exp_shift_batch<VEC>(eMa, xa, ga);
+            if (resid) exp_shift_batch<VEC>(eMb, xb, gb);
 #pragma unroll
-          for (int uu = 0; uu < U; ++uu) {
-              load_vec<Tin>(ra, e0 + (int64_t)uu * T * VEC, V, xa[uu]);
-              if (resid) load_vec<Tin>(rb, e0 + (int64_t)uu * T * VEC, V, xb[uu]);
-          }
-          if (eMa.tab && (!resid || eMb.tab)) {
+            for (int k = 0; k < VEC; ++k) {
+                if (xa[k] > NEG_MASKED) sa += ga[k];
+                if (resid && xb[k] > NEG_MASKED) sb += gb[k];
+            }
+        } else {
 #pragma unroll
-              for (int uu = 0; uu < U; ++uu) {
-                  double ga[VEC], gb[VEC];
-                  exp_shift_batch<VEC>(eMa, xa[uu], ga);
-                  if (resid) exp_shift_batch<VEC>(eMb, xb[uu], gb);
-#pragma unroll
-                  for (int k = 0; k < VEC; ++k) {
-                      if (xa[uu][k] > NEG_MASKED) sa += ga[k];
-                      if (resid && xb[uu][k] > NEG_MASKED) sb += gb[k];
-                  }
-              }
-          } else {
-#pragma unroll
-              for (int uu = 0; uu < U; ++uu) {
-#pragma unroll
-                  for (int k = 0; k < VEC; ++k) {
-                      if (xa[uu][k] > NEG_MASKED) sa += eMa(xa[uu][k]);
-                      if (resid && xb[uu][k] > NEG_MASKED) sb += eMb(xb[uu][k]);
-                  }
-              }
-          }
-      }
-  }
-  sa = block_sum_d(sa, sh);
-  if (resid) sb = block_sum_d(sb, sh);
-#ifdef MSD_PROF
-  long long _dx0 = clock64();
-  if (threadIdx.x == 0) g_tail_req[blockIdx.x][9] += (unsigned long long)_dx0;
-#endif
-  const double A = Ar.M + log(sa);
-  const double B0 = resid ? Br.M + log(sb) : 0.0;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    const double B = resid ? B0 : 0.0;
+            for (int k = 0; k < VEC; ++k) {
+                if (xa[k] > NEG_MASKED) sa += eMa(xa[k]);
+                if (resid && xb[k] > NEG_MASKED) sb += eMb(xb[k]);
+            }
+        }
+    }
+    *sa_out = block_sum_d(sa, sh);
+    *sb_out = resid ? block_sum_d(sb, sh) : 0.0;
+}
+
+// float64 mass of slice s of the (residual) weights with exact normalisers A, B -- whole CTA
+template <typename Tin>
+__device__ double exact_slice_mass(const Tin* ra, const Tin* rb, bool resid, int64_t V, int s, int vse, double A,
+                                   double B, const double* tab, TailShared& sh) {
+    constexpr int VEC = Elem<Tin>::VEC;
     ExpShift eA, eB;
     eA.init(tab, A);
     eB.init(tab, B);
-    for (int s = warp; s < C; s += NWARP) {
-        const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
-        double acc = 0.0;
-        constexpr int U = MSD_EXACT_U;
+    const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
+    double acc = 0.0;
 #pragma unroll 1
-        for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
-            float xa[U][VEC], xb[U][VEC];
+    for (int64_t e = s0 + (int64_t)threadIdx.x * VEC; e < s1; e += (int64_t)T * VEC) {
+        float xa[VEC], xb[VEC];
+        load_vec<Tin>(ra, e, s1, xa);
+        if (resid) load_vec<Tin>(rb, e, s1, xb);
+        if (eA.tab && (!resid || eB.tab)) {
+            double ga[VEC], gb[VEC];
+            exp_shift_batch<VEC>(eA, xa, ga);
+            if (resid) exp_shift_batch<VEC>(eB, xb, gb);
 #pragma unroll
-            for (int uu = 0; uu < U; ++uu) {
-                load_vec<Tin>(ra, e0 + (int64_t)uu * 32 * VEC, s1, xa[uu]);
-                if (resid) load_vec<Tin>(rb, e0 + (int64_t)uu * 32 * VEC, s1, xb[uu]);
-            }
-            if (eA.tab && (!resid || eB.tab)) {
-#pragma unroll
-                for (int uu = 0; uu < U; ++uu) {
-                    double ga[VEC], gb[VEC];
-                    exp_shift_batch<VEC>(eA, xa[uu], ga);
-                    if (resid) exp_shift_batch<VEC>(eB, xb[uu], gb);
-#pragma unroll
-                    for (int k = 0; k < VEC; ++k) {    // = wt(resid, za, zb, eA, eB)
-                        double w = 0.0;
-                        if (xa[uu][k] > NEG_MASKED) {
-                            w = ga[k];
-                            if (resid) {
-                                const double r = w - ((xb[uu][k] > NEG_MASKED) ? gb[k] : 0.0);
-                                w = r > 0.0 ? r : 0.0;
-                            }
-                        }
-                        acc += w;
+            for (int k = 0; k < VEC; ++k) {    // = wt(resid, za, zb, eA, eB)
+                double w = 0.0;
+                if (xa[k] > NEG_MASKED) {
+                    w = ga[k];
+                    if (resid) {
+                        const double r = w - ((xb[k] > NEG_MASKED) ? gb[k] : 0.0);
+                        w = r > 0.0 ? r : 0.0;
                     }
                 }
-            } else {
+                acc += w;
+            }
+        } else {
 #pragma unroll
-                for (int uu = 0; uu < U; ++uu) {
-#pragma unroll
-                    for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[uu][k], resid ? xb[uu][k] : NEG_CLAMP, eA, eB);
-                }
+            for (int k = 0; k < VEC; ++k) acc += wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, eA, eB);
+        }
+    }
+    return block_sum_d(acc, sh);
+}
+
+__device__ __forceinline__ uint32_t ld_acq(const uint32_t* p) { return ld_acquire_u32(p); }
+
+// Process chunks of job j until none is left in its current phase (whole CTA).  Returns after
+// the phase's chunks are all claimed.  Used by the requester and by helpers.
+template <typename Tin>
+__device__ __noinline__ void exact_work(JobBoard* bd, int j, uint32_t phase, TailShared& sh) {
+    ExactJob& J = bd->job[j];
+    // the job was written by another CTA during this kernel: L1-bypassing loads (ld.cg)
+    const Tin* ra = reinterpret_cast<const Tin*>(__ldcg(reinterpret_cast<const unsigned long long*>(&J.ra)));
+    const Tin* rb = reinterpret_cast<const Tin*>(__ldcg(reinterpret_cast<const unsigned long long*>(&J.rb)));
+    const double* tab = sizeof(Tin) == 2 ? sh.exptab : nullptr;
+    const bool resid = __ldcg(&J.resid) != 0;
+    const int Cj = __ldcg(&J.C), vse = __ldcg(&J.vse), chunk = __ldcg(&J.chunk);
+    const int64_t Vj = __ldcg(&J.V);
+    const double Ma = __ldcg(&J.Ma), Mb = __ldcg(&J.Mb);
+    const double Aj = phase == 2 ? __ldcg(&J.A) : 0.0, Bj = phase == 2 ? __ldcg(&J.B) : 0.0;
+    const int nch = phase == 1 ? EXJ_NCH : (Cj + EXJ_SPC - 1) / EXJ_SPC;
+    while (true) {
+        if (threadIdx.x == 0) sh.ex_chunk = (int)atomicAdd(phase == 1 ? &J.next1 : &J.next2, 1u);
+        __syncthreads();
+        const int ch = sh.ex_chunk;
+        __syncthreads();
+        if (ch >= nch) return;
+        if (phase == 1) {
+            const int64_t e0 = min(Vj, (int64_t)ch * chunk), e1 = min(Vj, e0 + chunk);
+            double sa, sb;
+            exact_norm_chunk<Tin>(ra, rb, resid, e0, e1, Ma, Mb, tab, sh, &sa, &sb);
+            if (threadIdx.x == 0) {
+                bd->part1[j][ch][0] = sa;
+                bd->part1[j][ch][1] = sb;
+                __threadfence();
+                atomicAdd(&J.done1, 1u);
+            }
+        } else {
+            for (int s = ch * EXJ_SPC; s < min(Cj, (ch + 1) * EXJ_SPC); ++s) {
+                const double m = exact_slice_mass<Tin>(ra, rb, resid, Vj, s, vse, Aj, Bj, tab, sh);
+                if (threadIdx.x == 0) bd->part2[j][s] = m;
+            }
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(&J.done2, 1u);
             }
         }
-        acc = warp_sum_d(acc);
-        if (lane == 0) sh.w[s] = acc;
+    }
+}
+
+// wait (thread 0 spins, the CTA then syncs) until *cnt == n; 2 s timeout -> false
+__device__ bool exact_wait(const uint32_t* cnt, uint32_t n, TailShared& sh) {
+    if (threadIdx.x == 0) {
+        const uint64_t t0 = globaltimer();
+        int ok = 1;
+        while (ld_acq(cnt) < n) {
+            if (globaltimer() - t0 > 2000000000ull) { ok = 0; break; }
+            __nanosleep(100);
+        }
+        sh.ex_ok = ok;
     }
     __syncthreads();
+    const bool ok = sh.ex_ok != 0;
+    __syncthreads();
+    return ok;
+}
+
+template <typename Tin>
+__device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin* rb, const RowStat& Ar,
+                              const RowStat& Br, int64_t V, int C, int vse, double u, TailShared& sh,
+                              bool* tie, bool* small, JobBoard* bd) {
+  constexpr int VEC = Elem<Tin>::VEC;
+#ifdef MSD_PROF
+  if (threadIdx.x == 0) g_tail_req[blockIdx.x][11] += (unsigned long long)clock64();
+#endif
+  // both rows into L2 up front (helpers and the slice-mass pass re-read them from L2)
+  prefetch_row_l2(ra, V);
+  if (resid) prefetch_row_l2(rb, V);
+  const double* tab = sizeof(Tin) == 2 ? sh.exptab : nullptr;
+  const int64_t chunk = ((V + EXJ_NCH - 1) / EXJ_NCH + VEC - 1) / VEC * VEC;
+  // post the job (or keep it local when the board is full: same chunks, computed here)
+  if (threadIdx.x == 0) {
+      int j = bd ? (int)atomicAdd(&bd->alloc, 1u) : EXJ_MAX;
+      sh.ex_job = j < EXJ_MAX ? j : -1;
+  }
+  __syncthreads();
+  const int jid = sh.ex_job;
+  __syncthreads();
+  double A, B0;
+  if (jid >= 0) {
+      ExactJob& J = bd->job[jid];
+      if (threadIdx.x == 0) {
+          J.ra = ra; J.rb = rb; J.Ma = Ar.M; J.Mb = Br.M; J.V = V;
+          J.resid = resid ? 1 : 0; J.C = C; J.vse = vse; J.chunk = (int32_t)chunk;
+          J.next1 = J.done1 = J.next2 = J.done2 = 0u;
+          __threadfence();
+          st_release_u32(&J.phase, 1u);
+      }
+      __syncthreads();
+      exact_work<Tin>(bd, jid, 1, sh);
+      if (!exact_wait(&J.done1, EXJ_NCH, sh)) return 0;
+      double sa = 0.0, sb = 0.0;
+      for (int c = 0; c < EXJ_NCH; ++c) { sa += __ldcg(&bd->part1[jid][c][0]); sb += __ldcg(&bd->part1[jid][c][1]); }
+      A = Ar.M + log(sa);
+      B0 = resid ? Br.M + log(sb) : 0.0;
+      if (threadIdx.x == 0) {
+          J.A = A; J.B = B0;
+          __threadfence();
+          st_release_u32(&J.phase, 2u);
+      }
+      __syncthreads();
+      exact_work<Tin>(bd, jid, 2, sh);
+      if (!exact_wait(&J.done2, (uint32_t)((C + EXJ_SPC - 1) / EXJ_SPC), sh)) return 0;
+      for (int s = threadIdx.x; s < C; s += T) sh.w[s] = __ldcg(&bd->part2[jid][s]);
+      if (threadIdx.x == 0) st_release_u32(&J.phase, 3u);
+      __syncthreads();
+  } else {
+      double sa = 0.0, sb = 0.0;
+      for (int c = 0; c < EXJ_NCH; ++c) {
+          const int64_t e0 = min(V, (int64_t)c * chunk), e1 = min(V, e0 + chunk);
+          double ca, cb;
+          exact_norm_chunk<Tin>(ra, rb, resid, e0, e1, Ar.M, Br.M, tab, sh, &ca, &cb);
+          sa += ca;
+          sb += cb;
+      }
+      A = Ar.M + log(sa);
+      B0 = resid ? Br.M + log(sb) : 0.0;
+      for (int s = 0; s < C; ++s) {
+          const double m = exact_slice_mass<Tin>(ra, rb, resid, V, s, vse, A, B0, tab, sh);
+          if (threadIdx.x == 0) sh.w[s] = m;
+      }
+      __syncthreads();
+  }
+#ifdef MSD_PROF
+  if (threadIdx.x == 0) g_tail_req[blockIdx.x][9] += (unsigned long long)clock64();
+#endif
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const double B = resid ? B0 : 0.0;
+    if (attempt == 1) {     // residual vanished: the slice masses of p, computed here
+        for (int s = 0; s < C; ++s) {
+            const double m = exact_slice_mass<Tin>(ra, rb, false, V, s, vse, A, 0.0, tab, sh);
+            if (threadIdx.x == 0) sh.w[s] = m;
+        }
+        __syncthreads();
+    }
 #ifdef MSD_PROF
     if (threadIdx.x == 0) g_tail_req[blockIdx.x][10] += (unsigned long long)clock64();
 #endif
+    const int lane = threadIdx.x & 31;
     double Z = 0.0;
     for (int s = lane; s < C; s += 32) Z += sh.w[s];
     Z = warp_sum_d(Z);
+    if (threadIdx.x < 32 && lane == 0) sh.red_d[0] = Z;
+    __syncthreads();
+    Z = sh.red_d[0];
+    __syncthreads();
     if (resid && Z < 1e-12) {   // residual vanished -> draw from p
         *small = true;
         resid = false;
@@ -722,6 +841,43 @@ __device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin*
     return y < 0 ? 0 : y;
   }
   return 0;
+}
+
+// Help with posted exact-draw jobs after this CTA's own request is done: claim chunks of any
+// job in its normaliser or slice-mass phase; linger only while every request has started
+// (so no waiting request is denied this slot) and some request is unfinished.
+template <typename Tin>
+__device__ __noinline__ void exact_help(JobBoard* bd, int64_t B, TailShared& sh) {
+    if (!bd) return;
+    const uint64_t t0 = globaltimer();
+    while (true) {
+        if (threadIdx.x == 0) {
+            int pick = -1, ph = 0;
+            const uint32_t n = min(ld_acq(&bd->alloc), (uint32_t)EXJ_MAX);
+            for (uint32_t j = 0; j < n && pick < 0; ++j) {
+                const uint32_t phs = ld_acq(&bd->job[j].phase);
+                if (phs == 1u && ld_acq(&bd->job[j].next1) < (uint32_t)EXJ_NCH) { pick = (int)j; ph = 1; }
+                else if (phs == 2u && ld_acq(&bd->job[j].next2) < (uint32_t)((__ldcg(&bd->job[j].C) + EXJ_SPC - 1) / EXJ_SPC)) { pick = (int)j; ph = 2; }
+            }
+            int go = 0;
+            if (pick < 0) {
+                const bool all_started = ld_acq(&bd->started) >= (uint32_t)B;
+                const bool all_done = ld_acq(&bd->finished) >= (uint32_t)B;
+                go = (!all_started || all_done || globaltimer() - t0 > 2000000000ull) ? -1 : 0;
+                if (go == 0) __nanosleep(1000);   // idle poll: keep the co-resident request's SM quiet
+            } else {
+                go = 1;
+            }
+            sh.ex_go = go;
+            sh.ex_pick = pick;
+            sh.ex_phase = ph;
+        }
+        __syncthreads();
+        const int go = sh.ex_go, pick = sh.ex_pick, ph = sh.ex_phase;
+        __syncthreads();
+        if (go < 0) return;
+        if (go > 0) exact_work<Tin>(bd, pick, (uint32_t)ph, sh);
+    }
 }
 
 // Block-wide copy of `bytes` (a multiple of 8) from global to shared memory with every load of
@@ -774,6 +930,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
     if (tid == 0 && b < 4096) g_tail_cta[b][0] = globaltimer();
 #endif
     if (tid == 0) {
+        if (p.board) atomicAdd(&p.board->started, 1u);
         sh.flags = 0;
         sh.exptab = p.exptab;
         int m1 = p.m0 ? p.m0[b] : K;
@@ -969,7 +1126,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
                 if (y < 0) {
                     exact = true;
                     tie = false;
-                    y = draw_exact<Tin>(resid, ra, rb, A, Bq, V, C, p.VSe, u, sh, &tie, &small);
+                    y = draw_exact<Tin>(resid, ra, rb, A, Bq, V, C, p.VSe, u, sh, &tie, &small, p.board);
                 }
             }
             if (tid == 0) {
@@ -1026,6 +1183,12 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
     unsigned long long* pm = reinterpret_cast<unsigned long long*>(p.partms) + (size_t)b * K * L * C;
     for (int t = tid; t < K * L * C; t += T) pm[t] = 0ull;
     TPROF(6)
+    // this request is done: help with other requests' exact draws while any is unfinished
+    if (tid == 0 && p.board) {
+        __threadfence();
+        atomicAdd(&p.board->finished, 1u);
+    }
+    exact_help<Tin>(p.board, p.B, sh);
 #ifdef MSD_PROF
     if (tid == 0 && b < 4096) g_tail_cta[b][1] = globaltimer();
 #endif

@@ -172,3 +172,23 @@ def test_every_subchain_of_a_four_model_pool(pre):
     ref = oracle.chain_verify([t[:, :, :pool.V].float().cpu().numpy() for t in levels], draft.cpu().numpy(),
                               ua.cpu().numpy(), ue.cpu().numpy(), tie_eps=1e-6, tie_eps_draw=1e-7)
     assert_parity(o, ref)
+
+
+@pytest.fixture
+def knobs():
+    yield api.debug_knobs
+    api.debug_knobs()
+
+
+def test_exact_draws_shared_across_ctas_are_deterministic(knobs):
+    # every draw exact: up to 2 jobs per request posted on the job board and split over the
+    # CTAs that finished their own request; chunk sums are combined in a fixed order, so the
+    # outputs must be bit-identical run to run and equal the oracle's
+    inp = _gauss("qwen25", B=40, V=50000)
+    knobs(exact_draws=True)
+    a = {k: v.clone() for k, v in _run(inp).items()}
+    b = _run(inp)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
+    assert_parity(b, run_oracle(inp))
+    assert (to_np(b)["flags"] & api.FLAG["EXACT_DRAW"]).sum() > 0
