@@ -163,6 +163,29 @@ msd_status msd_chain_verify(const msd_logits* levels, int32_t L, int32_t B, int3
 size_t msd_chain_verify_workspace(int32_t L, int32_t B, int32_t K, int64_t V);
 
 /* ---------------------------------------------------------------------------
+ * msd_chain_verify_proc -- msd_chain_verify with a logits processor (
+ * P:150 "LogitsProcessorList"): every level's distribution is softmax(z / T) instead of
+ * softmax(z) -- the acceptance ratios, residual / bonus draws, DTV, KL and stats are those of the
+ * temperature-scaled distributions; greedy mode is unchanged (argmax z / T = argmax z).  The
+ * logits are read once as before (the scale is applied inside the kernels, never written back).
+ * proc (host pointer, NULL = msd_chain_verify): temperature in (1e-6, 1e6]; top_k must be 0 and
+ * top_p 1 (or <= 0): top-k / top-p need a per-row threshold before the normaliser and are not
+ * implemented (MSD_E_ARG).  All other arguments as msd_chain_verify.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    float temperature;   /* T > 0; 1 = no scaling */
+    int32_t top_k;       /* 0 = off (only value accepted) */
+    float top_p;         /* 1 = off (only value accepted; <= 0 also means off) */
+} msd_processors;
+msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                                 const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                                 int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                                 int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                                 int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                                 msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                                 const msd_processors* proc, void* stream);
+
+/* ---------------------------------------------------------------------------
  * msd_kv_rollback -- batched rollback of each model's paged KV state
  * (§4.4: logical rollback of the last r_b entries, Eq. 8; physical
  * reclamation, Eq. 9, generalised to per-sequence release of whole blocks).

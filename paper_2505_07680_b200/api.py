@@ -44,6 +44,10 @@ class msd_pair_stats(ctypes.Structure):
 STATS_FIELDS = [f[0] for f in msd_pair_stats._fields_]
 
 
+class msd_processors(ctypes.Structure):
+    _fields_ = [("temperature", ctypes.c_float), ("top_k", ctypes.c_int32), ("top_p", ctypes.c_float)]
+
+
 class msd_paged_kv(ctypes.Structure):
     _fields_ = [("seq_len", ctypes.c_void_p), ("block_table", ctypes.c_void_p),
                 ("max_blocks", ctypes.c_int32), ("block_size", ctypes.c_int32),
@@ -67,6 +71,9 @@ def lib() -> ctypes.CDLL:
     L.msd_chain_verify.restype = i32
     L.msd_chain_verify.argtypes = [P, i32, i32, i32, i64, P, P, P, i32, i32, i32,
                                    P, P, P, P, P, P, P, P, P, P, sz, P]
+    L.msd_chain_verify_proc.restype = i32
+    L.msd_chain_verify_proc.argtypes = [P, i32, i32, i32, i64, P, P, P, i32, i32, i32,
+                                        P, P, P, P, P, P, P, P, P, P, sz, P, P]
     L.msd_verify_level.restype = i32
     L.msd_verify_level.argtypes = [msd_logits, msd_logits, i32, i32, i64, P, P, P, P, i32, i32,
                                    P, P, P, P, P, P, P, P, sz, P]
@@ -149,7 +156,7 @@ class ChainVerify:
     def __init__(self, levels: Sequence[torch.Tensor], draft: torch.Tensor, u_acc=None, u_emit=None,
                  *, V: Optional[int] = None, greedy=False, intermediate_bonus=True,
                  draft_fed: Optional[int] = None, pos_outputs=True, rollback=True, stats=True,
-                 ws: Optional[torch.Tensor] = None):
+                 ws: Optional[torch.Tensor] = None, temperature: Optional[float] = None):
         dev = draft.device
         _check(lib().msd_init(), "msd_init")   # one-time device setup, outside any graph capture
         self.L = len(levels)
@@ -180,7 +187,12 @@ class ChainVerify:
                       _ptr(self.commit_tok), _ptr(self.commit_len), _ptr(self.rollback),
                       _ptr(self.pos_dtv), _ptr(self.pos_kl), _ptr(self.stats), _ptr(self.flags),
                       _ptr(self.ws), self.ws.numel()]
-        self._fn = lib().msd_chain_verify
+        if temperature is None:
+            self._fn = lib().msd_chain_verify
+        else:     # logits processor (msd_chain_verify_proc): softmax(z / T) at every level
+            self._proc = msd_processors(float(temperature), 0, 1.0)
+            self._args.append(ctypes.byref(self._proc))
+            self._fn = lib().msd_chain_verify_proc
 
     def __call__(self, stream=None):
         _check(self._fn(*self._args, _stream(stream)), "msd_chain_verify")

@@ -137,6 +137,7 @@ struct Engine {
     void* ws;
     size_t ws_bytes;
     cudaStream_t stream;
+    float inv_temp;     // logits processor: 1 / temperature (1 = none)
 };
 
 msd_status validate_levels(const msd_logits* lv, int32_t L, int32_t K, int64_t V, int32_t ibonus,
@@ -194,6 +195,7 @@ msd_status run_engine(const Engine& E) {
     cp.board = reinterpret_cast<JobBoard*>(ws + w.board);
     cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
     cp.dbg = g_knobs.core_dbg;
+    cp.inv_temp = E.inv_temp;
 
     TailParams tp;
     memset(&tp, 0, sizeof(tp));
@@ -209,6 +211,7 @@ msd_status run_engine(const Engine& E) {
     tp.partials = cp.partials; tp.partms = cp.partms; tp.resid = cp.resid;
     tp.cnt = cp.cnt;
     tp.board = cp.board;
+    tp.inv_temp = E.inv_temp;
     tp.z_safe = g_knobs.z_safe;                  // exact draws below this residual mass (R4)
     tp.exact_all = g_knobs.exact_draws;
     {
@@ -267,6 +270,26 @@ msd_status msd_chain_verify(const msd_logits* levels, int32_t L, int32_t B, int3
                             int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
                             msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
                             void* stream) {
+    return msd_chain_verify_proc(levels, L, B, K, V, draft_tok, u_acc, u_emit, mode, intermediate_bonus,
+                                 draft_fed, n_acc, m_cand, commit_tok, commit_len, rollback, pos_dtv,
+                                 pos_kl, stats, flags, ws, ws_bytes, nullptr, stream);
+}
+
+msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                                 const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                                 int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                                 int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                                 int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                                 msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                                 const msd_processors* proc, void* stream) {
+    float inv_temp = 1.f;
+    if (proc) {
+        if (!(proc->temperature > 0.f) || !(proc->temperature <= 1e6f) || !(1.f / proc->temperature <= 1e6f))
+            return fail(MSD_E_ARG, "temperature %g outside (1e-6, 1e6]", (double)proc->temperature);
+        if (proc->top_k != 0 || !(proc->top_p >= 1.f || proc->top_p <= 0.f))
+            return fail(MSD_E_ARG, "top_k / top_p are not supported (pass 0 / 1)");
+        inv_temp = 1.f / proc->temperature;
+    }
     if (!levels) return fail(MSD_E_ARG, "levels is NULL");
     if (L < 2 || L > MAXL) return fail(MSD_E_ARG, "L=%d outside [2,%d]", L, MAXL);
     if (B < 0 || K < 1 || K + L > MAXC) return fail(MSD_E_ARG, "bad B=%d / K=%d (need K+L <= 32)", B, K);
@@ -305,6 +328,7 @@ msd_status msd_chain_verify(const msd_logits* levels, int32_t L, int32_t B, int3
     E.pos_dtv = pos_dtv; E.pos_kl = pos_kl; E.stats = stats; E.flags = flags;
     E.ws = ws; E.ws_bytes = ws_bytes;
     E.stream = reinterpret_cast<cudaStream_t>(stream);
+    E.inv_temp = inv_temp;
     return run_engine(E);
 }
 
@@ -349,6 +373,7 @@ msd_status msd_verify_level(msd_logits q, msd_logits p, int32_t B, int32_t K, in
     E.pos_dtv = pos_dtv; E.pos_kl = pos_kl; E.stats = stats; E.flags = flags;
     E.ws = ws; E.ws_bytes = ws_bytes;
     E.stream = reinterpret_cast<cudaStream_t>(stream);
+    E.inv_temp = 1.f;
     return run_engine(E);
 }
 

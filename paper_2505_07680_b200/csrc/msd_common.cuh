@@ -383,7 +383,7 @@ __device__ __forceinline__ float2 exp2_pair_fma(float2 x) {
 // that does it gets bit-identical results).  Executed by one full warp.  The slice KL
 // numerators K_s = sum_{v in s} e^{z_v - m_s} (z_v - z'_v) (raw logit differences) are
 // rescaled to the row maximum in float64: K = sum_s K_s e^{m_s - M}.
-__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out) {
+__device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out, double sc = 1.0) {
     const int lane = threadIdx.x & 31;
     float m = -INFINITY;
     for (int s = lane; s < C; s += 32) m = fmaxf(m, parts[s].m);
@@ -394,7 +394,7 @@ __device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out
     for (int s = lane; s < C; s += 32) {
         float ms = parts[s].m;
         double Ss = parts[s].S;
-        double f = dexp_neg((double)ms - (double)m);
+        double f = dexp_neg(((double)ms - (double)m) * sc);   // sc = 1 / temperature
         S += Ss * f;
         Kl += parts[s].Kl * f;
         if (ms == m) am = min(am, parts[s].amax);
@@ -407,7 +407,7 @@ __device__ inline RowStat combine_row(const Partial* parts, int C, double* K_out
     RowStat r;
     r.M = (double)m;
     r.S = S;
-    r.lse = (double)m + log(S);
+    r.lse = (double)m * sc + log(S);        // scaled units
     r.amax = am == 0x7fffffff ? 0 : am;
     r.bad = (bad || !(m > NEG_MASKED) || !isfinite(S) || !(m < INFINITY)) ? 1 : 0;
     if (K_out) *K_out = Kl;

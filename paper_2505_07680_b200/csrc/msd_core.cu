@@ -271,10 +271,10 @@ __device__ __noinline__ void repair_stage(Tin* stage, int rs, const LevelDesc& l
 // returned too); `clamp`: the -1e30 clamp first (-inf -> p = 0 without 0 * inf), NaN kept.
 constexpr int CH = 16;
 template <typename Tin>
-__device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, float* e, float2* y) {
+__device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, float* e, float2* y, float l2s) {
     const float nm = -m;
     const float2 nm2 = make_float2(nm, nm);
-    const float2 l2e = make_float2(LOG2E, LOG2E);
+    const float2 l2e = make_float2(l2s, l2s);     // log2(e) / temperature
 #pragma unroll
     for (int pp = 0; pp < CH / 2; ++pp) {
         float2 yy;
@@ -306,7 +306,7 @@ __device__ __forceinline__ void row_exp(const uint4* raw, float m, bool clamp, f
 // e and y = z - m of quarter h (8 of the thread's 32 elements) of one row of a ring stage
 template <typename Tin>
 __device__ __forceinline__ void half_exp(const Tin* row, int rg, int lane, int h, float m, bool clamp, float* e,
-                                         float2* y) {
+                                         float2* y, float l2s) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NVH = 8 / VEC;        // vectors per half: 1 (bf16) or 2 (f32)
     uint4 raw[NVH];
@@ -315,7 +315,7 @@ __device__ __forceinline__ void half_exp(const Tin* row, int rg, int lane, int h
         raw[jv] = *reinterpret_cast<const uint4*>(row + vec_index<Tin>(rg, lane, h * NVH + jv));
     const float nm = -m;
     const float2 nm2 = make_float2(nm, nm);
-    const float2 l2e = make_float2(LOG2E, LOG2E);
+    const float2 l2e = make_float2(l2s, l2s);     // log2(e) / temperature
 #pragma unroll
     for (int pp = 0; pp < 4; ++pp) {
         float2 yy;
@@ -400,6 +400,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int C = p.C;
     const int VSe = p.VSe;
+    // temperature T (logits processor): every exponent is (z - m) / T, sc = 1 / T.  Records
+    // and Partials keep raw maxima (the tail scales its exponents the same way); the Partials' KL
+    // numerator is sum e (z_l - z_{l-1}) / T.
+    const float sc = p.inv_temp, l2s = LOG2E * p.inv_temp;
     const int RS = p.rs;                    // ring row stride (entries)
     const int S = p.stages;
     const int PP = p.pat_p, PT = p.pat_t;
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         float msl = wm;
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
-        float f = wm == msl ? 1.f : ex2f((wm - msl) * LOG2E);
+        float f = wm == msl ? 1.f : ex2f((wm - msl) * l2s);
         if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
         // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
         float Sx = Sw * f, Kx = (l > 0 && f != 0.f) ? f * Kw : 0.f;
@@ -570,10 +574,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
         if (pub_lane) {
             Partial pr;
-            pr.m = msl;
+            pr.m = msl;                                   // raw units (the tail scales exponents)
             pr.amax = GREEDY ? ax : 0;
             pr.S = Sd;
-            pr.Kl = (double)Kx;
+            pr.Kl = (double)Kx * (double)sc;
             p.partials[idx] = pr;
         }
 #if MSD_PUB_LATE
@@ -669,7 +673,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         for (int l = 0; l < L; ++l) {
                             float e[8];
                             float2 y[4];
-                            half_exp<Tin>(stage + (size_t)l * RS, rg, lane, h, wm[l], clamp, e, y);
+                            half_exp<Tin>(stage + (size_t)l * RS, rg, lane, h, wm[l], clamp, e, y, l2s);
                             const float2 e01 = __fadd2_rn(make_float2(e[0], e[1]), make_float2(e[2], e[3]));
                             const float2 e23 = __fadd2_rn(make_float2(e[4], e[5]), make_float2(e[6], e[7]));
                             s2[l] = __fadd2_rn(s2[l], __fadd2_rn(e01, e23));
@@ -899,7 +903,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                                                                               vec_index<Tin>(v, lane, ch * NVC + jv));
                                 float e[CH];
                                 float2 y[CH / 2];
-                                row_exp<Tin>(raw, wm[l], clamp, e, y);
+                                row_exp<Tin>(raw, wm[l], clamp, e, y, l2s);
                                 if (l > 0) pair(l, e, eprev);
 #pragma unroll
                                 for (int kk = 0; kk < CH; ++kk) eprev[kk] = e[kk];
@@ -1045,7 +1049,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const unsigned long long r = fb[l * C + t];
                     const float vm = __uint_as_float((uint32_t)r);
                     if (vm > NEG_MASKED)
-                        Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), ex2f((vm - Rl[l]) * LOG2E), Sl[l]);
+                        Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), ex2f((vm - Rl[l]) * l2s), Sl[l]);
                 }
             }
 #pragma unroll
@@ -1074,7 +1078,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         const unsigned long long r = fb[l * C + t];
                         const float vm = __uint_as_float((uint32_t)r);
                         if (vm > NEG_MASKED)
-                            Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma((vm - Rl[l]) * LOG2E), Sl[l]);
+                            Sl[l] = fmaf(__uint_as_float((uint32_t)(r >> 32)), exp2f_fma((vm - Rl[l]) * l2s), Sl[l]);
                     }
                 }
 #pragma unroll
@@ -1092,8 +1096,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     for (int r = 1; r < L; ++r)
                         if (r == l) { Ma = Rl[r]; Sa = Sl[r]; Mb = Rl[r - 1]; Sb = Sl[r - 1]; }
                     const float wa = c.wmx[k][l][w], wb = c.wmx[k][l - 1][w];
-                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? ex2f((wa - Ma) * LOG2E) : 0.f;
-                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? ex2f((wb - Mb) * LOG2E) : 0.f;
+                    const float ca = (wa > NEG_MASKED && Ma > NEG_MASKED) ? ex2f((wa - Ma) * l2s) : 0.f;
+                    const float cb = (wb > NEG_MASKED && Mb > NEG_MASKED) ? ex2f((wb - Mb) * l2s) : 0.f;
                     const bool skip = !(ca > 0.f) || !(Sa > 0.f) || !(Sb > 0.f) || !isfinite(Sa) || !isfinite(Sb) ||
                                       !isfinite(ca) || !isfinite(cb);
                     WF wf;

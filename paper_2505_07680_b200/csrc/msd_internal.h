@@ -40,7 +40,8 @@ struct CoreParams {
     uint32_t* err;
     JobBoard* board;             // reset by CTA 0 before the roles start (the tail's exact-draw jobs)
     unsigned long long* trace;   // debug: 16 globaltimer stamps per item, or NULL
-    int32_t dbg;                 // debug isolation mode (MSD_CORE_DBG): 0 = normal
+    int32_t dbg;                 // debug isolation mode (msd_debug_set_knobs): 0 = normal
+    float inv_temp;              // 1 / temperature of the logits processor (1 = none)
 };
 
 // exp of every bf16 value in float64 (65536 entries), filled once per device by msd_init (or
@@ -76,6 +77,7 @@ struct TailParams {
     int32_t prefetch;   // set by launch_tail: partials + residuals of a request fit in shared memory
     const double* exptab;   // exp of every bf16 value (exact-draw path), from exp_table()
     JobBoard* board;        // exact-draw work sharing (reset by the core kernel)
+    float inv_temp;         // 1 / temperature: the tail works on z / T (1 = none)
 };
 
 struct PoolParams {          // SimScore bootstrap (msd_pool.cu)

@@ -107,6 +107,11 @@ __device__ __forceinline__ float block_max_f(float v, TailShared& sh) {
     return t;
 }
 
+// Temperature (logits processor): the distributions are softmax(z / T).  The tail keeps
+// logits and maxima in raw units and applies sc = 1 / T inside every exponent, (z - M) sc, in
+// float64 where the decision depends on it; a normaliser `lse` is in scaled units (M sc + log S).
+__shared__ float s_sc;               // 1 / T for this launch (set by thread 0 at kernel start)
+
 // Load this thread's ET elements of slice s of a row (same mapping as the core),
 // clamped; out-of-row entries are NEG_CLAMP.
 template <typename Tin>
@@ -176,7 +181,7 @@ __device__ bool slice_partial_bf16(const __nv_bfloat16* row, int64_t s0, int64_t
     m = __shfl_sync(0xffffffffu, m, 0);
     if (!(m > NEG_MASKED) || !(m < INFINITY)) return false;
     const float nm = -m;
-    const float2 l2e = make_float2(LOG2E, LOG2E);
+    const float2 l2e = make_float2(LOG2E * s_sc, LOG2E * s_sc);   // (z - m) / T
     double S = 0.0;
     int am = 0x7fffffff;
     for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
@@ -260,13 +265,13 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShar
 #pragma unroll
                 for (int k = 1; k < VEC; ++k) mv = fmaxf(mv, x[uu][k]);
                 if (mv > m) {      // new running maximum: rescale (first index of the maximum kept)
-                    S *= dexp_neg((double)m - (double)mv);
+                    S *= dexp_neg(((double)m - (double)mv) * (double)s_sc);
                     m = mv;
                     am = 0x7fffffff;
                 }
                 float sv = 0.f;
 #pragma unroll
-                for (int k = 0; k < VEC; ++k) sv += ex2f((x[uu][k] - m) * LOG2E);
+                for (int k = 0; k < VEC; ++k) sv += ex2f((x[uu][k] - m) * (LOG2E * s_sc));
                 S += (double)sv;
 #pragma unroll
                 for (int k = 0; k < VEC; ++k)
@@ -275,7 +280,7 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShar
         }
         // combine the lanes (fixed order)
         const float ms = warp_max(m);
-        double f = dexp_neg((double)m - (double)ms);
+        double f = dexp_neg(((double)m - (double)ms) * (double)s_sc);
         if (!(m > NEG_MASKED)) f = (ms > NEG_MASKED) ? 0.0 : 1.0;
         double Ss = warp_sum_d(S * f);
         const int a = warp_min_i(m == ms ? am : 0x7fffffff);
@@ -296,7 +301,7 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShar
         int am = 0x7fffffff;
         bool bad = false;
         for (int s = lane; s < C; s += 32) {
-            S += sh.part[s].S * dexp_neg((double)sh.part[s].m - (double)m);
+            S += sh.part[s].S * dexp_neg(((double)sh.part[s].m - (double)m) * (double)s_sc);
             if (sh.part[s].m == m) am = min(am, sh.part[s].amax);
             if (isnan(sh.part[s].m) || isnan(sh.part[s].S)) bad = true;
         }
@@ -305,7 +310,7 @@ __device__ RowStat row_stats(const Tin* row, int64_t V, int C, int vse, TailShar
         bad = __any_sync(0xffffffffu, bad);
         if (lane == 0) {
             RowStat r;
-            r.M = m; r.S = S; r.lse = (double)m + log(S);
+            r.M = m; r.S = S; r.lse = (double)m * (double)s_sc + log(S);
             r.amax = am == 0x7fffffff ? 0 : am;
             r.bad = (bad || !(m > NEG_MASKED) || !isfinite(S) || !(m < INFINITY)) ? 1 : 0;
             res = r;
@@ -343,8 +348,8 @@ __device__ void pair_resid(const Tin* ra, const Tin* rb, const RowStat& A, const
                 float av = 0.f;
 #pragma unroll
                 for (int k = 0; k < VEC; ++k) {
-                    const float ea = ex2f((xa[uu][k] - Ma) * LOG2E);
-                    const float eb = ex2f((xb[uu][k] - Mb) * LOG2E);
+                    const float ea = ex2f((xa[uu][k] - Ma) * (LOG2E * s_sc));
+                    const float eb = ex2f((xb[uu][k] - Mb) * (LOG2E * s_sc));
                     float t = fmaf(-eb, rh, ea);
                     t = fmaf(-eb, rl, t);
                     av += fmaxf(t, 0.f);
@@ -386,12 +391,15 @@ __device__ __forceinline__ void load16(const Tin* row, int64_t e0, int64_t Vend,
 // made the exact draw instruction-cache bound: 'no_inst' stalls at the table gathers)
 __device__ __noinline__ double dexp_neg_cold(double x) { return dexp_neg(x); }
 
+// exp(z sc - S) for a raw logit z and a scaled offset S (sc = 1 / T; the bf16 table only when
+// sc = 1: it holds exp of raw bf16 values)
 struct ExpShift {
-    const double* tab;   // NULL: no table (f32 logits)
-    double S, eS;
+    const double* tab;   // NULL: no table (f32 logits, or a temperature)
+    double S, eS, sc;
     __device__ void init(const double* t, double s_) {
-        tab = (t && fabs(s_) < 700.0) ? t : nullptr;
+        tab = (t && fabs(s_) < 700.0 && s_sc == 1.f) ? t : nullptr;
         S = s_;
+        sc = (double)s_sc;
         eS = tab ? exp(-s_) : 0.0;
     }
     __device__ __forceinline__ double operator()(float z) const {
@@ -399,7 +407,7 @@ struct ExpShift {
             const double t = __ldg(tab + (__float_as_uint(z) >> 16));
             if (t == t) return t * eS;      // NaN entry: outside the table's range
         }
-        return dexp_neg_cold((double)z - S);     // z <= max <= S: argument <= 0
+        return dexp_neg_cold((double)z * sc - S);     // z sc <= max sc <= S: argument <= 0
     }
 };
 
@@ -410,14 +418,15 @@ __device__ __forceinline__ void exp_shift_batch(const ExpShift& es, const float*
 #pragma unroll
     for (int k = 0; k < N; ++k) out[k] = __ldg(es.tab + (__float_as_uint(z[k]) >> 16));
 #pragma unroll
-    for (int k = 0; k < N; ++k) out[k] = (out[k] == out[k]) ? out[k] * es.eS : dexp_neg_cold((double)z[k] - es.S);
+    for (int k = 0; k < N; ++k) out[k] = (out[k] == out[k]) ? out[k] * es.eS : dexp_neg_cold((double)z[k] * es.sc - es.S);
 }
 
 __device__ __forceinline__ double wt(bool resid, float za, float zb, double A, double B) {
     if (!(za > NEG_MASKED)) return 0.0;
-    const double pa = dexp_neg((double)za - A);     // z <= max <= lse: argument <= 0
+    const double sc = (double)s_sc;
+    const double pa = dexp_neg((double)za * sc - A);     // z sc <= max sc <= lse: argument <= 0
     if (!resid) return pa;
-    const double qb = (zb > NEG_MASKED) ? dexp_neg((double)zb - B) : 0.0;
+    const double qb = (zb > NEG_MASKED) ? dexp_neg((double)zb * sc - B) : 0.0;
     const double r = pa - qb;
     return r > 0.0 ? r : 0.0;
 }
@@ -496,9 +505,9 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
         for (int k = 0; k < ET; ++k) {
             float wk = 0.f;
             if (xa[k] > NEG_MASKED) {
-                wk = ex2f(((xa[k] - Ah) - Al) * LOG2E);
+                wk = ex2f(((xa[k] * s_sc - Ah) - Al) * LOG2E);     // fast path: fp32 z / T (margins)
                 if (resid) {
-                    const float qk = xb[k] > NEG_MASKED ? ex2f(((xb[k] - Bh) - Bl) * LOG2E) : 0.f;
+                    const float qk = xb[k] > NEG_MASKED ? ex2f(((xb[k] * s_sc - Bh) - Bl) * LOG2E) : 0.f;
                     wk = fmaxf(wk - qk, 0.f);
                 }
             }
@@ -612,8 +621,8 @@ __device__ void exact_norm_chunk(const Tin* ra, const Tin* rb, bool resid, int64
                                  double Mb, const double* tab, TailShared& sh, double* sa_out, double* sb_out) {
     constexpr int VEC = Elem<Tin>::VEC;
     ExpShift eMa, eMb;
-    eMa.init(tab, Ma);
-    eMb.init(tab, Mb);
+    eMa.init(tab, Ma * (double)s_sc);     // raw maxima -> scaled offsets
+    eMb.init(tab, Mb * (double)s_sc);
     double sa = 0.0, sb = 0.0;
 #pragma unroll 1
     for (int64_t e = e0 + (int64_t)threadIdx.x * VEC; e < e1; e += (int64_t)T * VEC) {
@@ -779,8 +788,8 @@ __device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin*
       if (!exact_wait(&J.done1, EXJ_NCH, sh)) return 0;
       double sa = 0.0, sb = 0.0;
       for (int c = 0; c < EXJ_NCH; ++c) { sa += __ldcg(&bd->part1[jid][c][0]); sb += __ldcg(&bd->part1[jid][c][1]); }
-      A = Ar.M + log(sa);
-      B0 = resid ? Br.M + log(sb) : 0.0;
+      A = Ar.M * (double)s_sc + log(sa);
+      B0 = resid ? Br.M * (double)s_sc + log(sb) : 0.0;
       if (threadIdx.x == 0) {
           J.A = A; J.B = B0;
           __threadfence();
@@ -801,8 +810,8 @@ __device__ __noinline__ int32_t draw_exact(bool resid, const Tin* ra, const Tin*
           sa += ca;
           sb += cb;
       }
-      A = Ar.M + log(sa);
-      B0 = resid ? Br.M + log(sb) : 0.0;
+      A = Ar.M * (double)s_sc + log(sa);
+      B0 = resid ? Br.M * (double)s_sc + log(sb) : 0.0;
       for (int s = 0; s < C; ++s) {
           const double m = exact_slice_mass<Tin>(ra, rb, resid, V, s, vse, A, B0, tab, sh);
           if (threadIdx.x == 0) sh.w[s] = m;
@@ -931,6 +940,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
 #endif
     if (tid == 0) {
         if (p.board) atomicAdd(&p.board->started, 1u);
+        s_sc = p.inv_temp;
         sh.flags = 0;
         sh.exptab = p.exptab;
         int m1 = p.m0 ? p.m0[b] : K;
@@ -965,7 +975,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
         const int i = r / L, l = r % L;
         double Kl;
         const Partial* pp = part_b + ((size_t)i * L + l) * C;
-        RowStat rs = combine_row(pp, C, &Kl);   // slice KL numerators are raw: sum e (z_l - z_{l-1})
+        RowStat rs = combine_row(pp, C, &Kl, (double)s_sc);   // KL numerators: sum e (z_l - z_{l-1}) / T
         if (lane == 0) { sh.row[i][l] = rs; sh.kl[i][l] = Kl; }
     }
     __syncthreads();
@@ -1025,7 +1035,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
                     } else if (!(zb > NEG_MASKED)) {
                         acc = true;
                     } else {
-                        const double lr = ((double)za - (double)zb) - (A.lse - Bq.lse);
+                        const double lr = ((double)za - (double)zb) * (double)s_sc - (A.lse - Bq.lse);
                         const double r = lr >= 0.0 ? 1.0 : exp(lr);
                         acc = u < r;
                         tie = fabs(u - r) < TIE_EPS;
@@ -1111,7 +1121,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
                     const Partial* P = part_b + ((size_t)pos * L + l) * C;
                     for (int s = tid; s < C; s += T) {
                         const Partial pr = pos < K ? P[s] : sh.part[s];
-                        sh.w[s] = pr.S * dexp_neg((double)pr.m - A.M) / A.S;
+                        sh.w[s] = pr.S * dexp_neg(((double)pr.m - A.M) * (double)s_sc) / A.S;
                     }
                     __syncthreads();
                 }

@@ -61,11 +61,12 @@ def compare(gpu, ref, requests=None, check_rollback=True):
     return rep
 
 
-def assert_parity(gpu, ref, requests=None, check_rollback=True, max_near_tie_frac=0.1):
+def assert_parity(gpu, ref, requests=None, check_rollback=True, max_near_tie_frac=0.1, check_divergence=True):
     rep = compare(gpu, ref, requests, check_rollback)
     assert not rep["mismatch"], f"token/length mismatch outside near ties: requests {rep['mismatch'][:20]}"
-    assert rep["dtv_err"] <= 0, f"DTV outside tolerance by {rep['dtv_err']}"
-    assert rep["kl_err"] <= 0, f"KL outside tolerance by {rep['kl_err']}"
+    if check_divergence:
+        assert rep["dtv_err"] <= 0, f"DTV outside tolerance by {rep['dtv_err']}"
+        assert rep["kl_err"] <= 0, f"KL outside tolerance by {rep['kl_err']}"
     n = ref["out_len"].shape[0]
     assert rep["near_tie"] <= max(2, max_near_tie_frac * n), rep
     return rep
