@@ -286,6 +286,22 @@ msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, i
                             float* q_tok, uint32_t* flags, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * msd_lmhead_lse -- the step before the path, fused (Eq. 1
+ * "softmax(h_t W)"): for every row r of H the normaliser LSE_r = log sum_v exp(z_rv) of the
+ * logits z = H W^T and the candidate's logit z_r,cand[r], computed by a tcgen05 GEMM whose
+ * epilogue reduces each accumulator tile on the fly -- the M x V logits are never written.
+ * H [M][D] bf16 row-major (hidden states), W [V][D] bf16 row-major (the lm_head weight, nn.Linear
+ * layout); D a multiple of 64; 16-byte aligned.  cand [M] int32 (NULL ok; -1 / out of range ->
+ * z_cand NaN); outputs lse [M] f32, z_cand [M] f32 (NULL ok).  Arithmetic: bf16 products with
+ * fp32 tensor-core accumulation (the logits a bf16 lm_head produces before rounding), online
+ * (max, sum) in fp32 per 32 columns and float64 across them.  ws: >= msd_lmhead_workspace(M, V)
+ * bytes (per-row partial records).  Asynchronous on `stream`.
+ * ------------------------------------------------------------------------- */
+size_t msd_lmhead_workspace(int32_t M, int64_t V);
+msd_status msd_lmhead_lse(const void* H, const void* W, int32_t M, int32_t D, int64_t V, const int32_t* cand,
+                          float* lse, float* z_cand, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics.
  * msd_last_error: thread-local message for the last non-OK status of this thread.
  * msd_prof_enable(1): record CUDA events around every msd_core launch (the

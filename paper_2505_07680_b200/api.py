@@ -98,6 +98,10 @@ def lib() -> ctypes.CDLL:
     L.msd_abi_version.restype = i32
     L.msd_init.restype = i32
     L.msd_init.argtypes = []
+    L.msd_lmhead_workspace.restype = sz
+    L.msd_lmhead_workspace.argtypes = [i32, i64]
+    L.msd_lmhead_lse.restype = i32
+    L.msd_lmhead_lse.argtypes = [P, P, i32, i32, i64, P, P, P, P, sz, P]
     L.msd_prof_enable.restype = i32
     L.msd_prof_enable.argtypes = [i32]
     L.msd_prof_read.restype = i32
@@ -350,6 +354,22 @@ def debug_knobs(pat_t=-1, pat_r=-1, stages=-1, core_dbg=0, exact_draws=False, z_
     arguments to restore the release defaults."""
     _check(lib().msd_debug_set_knobs(int(pat_t), int(pat_r), int(stages), int(core_dbg),
                                      int(bool(exact_draws)), float(z_safe)), "msd_debug_set_knobs")
+
+
+def lmhead_lse(H: torch.Tensor, W: torch.Tensor, cand: Optional[torch.Tensor] = None, stream=None) -> dict:
+    """msd_lmhead_lse: row normalisers of H W^T (and the candidate logits) without writing the
+    logits.  H [M, D] bf16, W [V, D] bf16 (contiguous)."""
+    if H.dtype != torch.bfloat16 or W.dtype != torch.bfloat16 or not H.is_contiguous() or not W.is_contiguous():
+        raise MsdError("H and W must be contiguous bf16")
+    M, D = H.shape
+    V = W.shape[0]
+    dev = H.device
+    lse = torch.empty(M, dtype=torch.float32, device=dev)
+    zc = torch.empty(M, dtype=torch.float32, device=dev)
+    ws = torch.empty(max(1, int(lib().msd_lmhead_workspace(M, V))), dtype=torch.uint8, device=dev)
+    _check(lib().msd_lmhead_lse(H.data_ptr(), W.data_ptr(), M, D, V, _ptr(cand), lse.data_ptr(), zc.data_ptr(),
+                                ws.data_ptr(), ws.numel(), _stream(stream)), "msd_lmhead_lse")
+    return dict(lse=lse, z_cand=zc, ws=ws)
 
 
 def prof_enable(on=True):

@@ -463,6 +463,35 @@ msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, i
     return MSD_OK;
 }
 
+size_t msd_lmhead_workspace(int32_t M, int64_t V) {
+    if (M < 1 || V < 1) return 0;
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return lmhead_workspace(M, V, nsm > 0 ? nsm : 148);
+}
+
+msd_status msd_lmhead_lse(const void* H, const void* W, int32_t M, int32_t D, int64_t V, const int32_t* cand,
+                          float* lse, float* z_cand, void* ws, size_t ws_bytes, void* stream) {
+    if (M < 0 || D < 64 || D % 64 || V < 1 || V > ((int64_t)1 << 31) - 1)
+        return fail(MSD_E_ARG, "bad M=%d / D=%d (multiple of 64) / V=%lld", M, D, (long long)V);
+    if (M == 0) return MSD_OK;
+    if (!H || !W || !lse || !ws) return fail(MSD_E_ARG, "H, W, lse and ws are required");
+    if (((uintptr_t)H) % 16 || ((uintptr_t)W) % 16) return fail(MSD_E_ALIGN, "H and W must be 16-byte aligned");
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    if (ws_bytes < msd_lmhead_workspace(M, V)) return fail(MSD_E_WORKSPACE, "workspace too small");
+    LmHeadParams p;
+    p.H = H; p.W = W; p.M = M; p.D = D; p.V = V; p.cand = cand; p.lse = lse; p.z_cand = z_cand;
+    p.ws = ws; p.ws_bytes = ws_bytes;
+    {
+        std::lock_guard<std::mutex> g(g_prof.mu);
+        g_prof.total_launches += 2;
+    }
+    cudaError_t e = launch_lmhead(p, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "msd_lmhead launch");
+    return MSD_OK;
+}
+
 msd_status msd_debug_set_trace(void* dev_buf, size_t bytes) {
     g_trace = reinterpret_cast<unsigned long long*>(dev_buf);
     g_trace_items = dev_buf ? bytes / 128 : 0;

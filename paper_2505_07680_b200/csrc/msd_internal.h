@@ -109,6 +109,18 @@ struct RollbackParams {
     uint32_t* flags;
 };
 
+struct LmHeadParams {        // fused lm_head GEMM + row normaliser (msd_lmhead.cu)
+    const void* H;           // [M][D] bf16
+    const void* W;           // [V][D] bf16
+    int32_t M, D;
+    int64_t V;
+    const int32_t* cand;     // [M] or NULL
+    float* lse;              // [M]
+    float* z_cand;           // [M] or NULL
+    void* ws;
+    size_t ws_bytes;
+};
+
 // Test / diagnostic overrides (msd_debug_set_knobs); the defaults are the release behaviour.
 struct DebugKnobs {
     int32_t pat_t = -1, pat_r = -1, stages = -1, core_dbg = 0, exact_draws = 0;
@@ -122,5 +134,7 @@ cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_rollback(const RollbackParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_draft(const DraftParams& p, int bf16, cudaStream_t s);
+cudaError_t launch_lmhead(const LmHeadParams& p, cudaStream_t s);
+size_t lmhead_workspace(int32_t M, int64_t V, int nsm);
 
 }  // namespace msd
