@@ -68,8 +68,13 @@ constexpr int NFETCH = MSD_NFETCH;
 // warp W_P2 + v serves regions v and v + 4 (quadrant v): both bases are multiples of 4.
 constexpr int W_PROD = 0, W_PUB = 1, W_FETCH0 = 2, W_RED = W_FETCH0 + NFETCH;
 constexpr int W_P2 = (W_RED + 1 + 3) / 4 * 4, W_P1 = W_P2 + NCW2;   // (4 with one fetcher: 28 warps, 72 registers)
-constexpr int NG1 = 2;                 // pass-1 warp groups: group g processes items j = g mod NG1
-constexpr int CORE_THREADS = (W_P1 + NG1 * NCW) * 32;
+#ifndef MSD_SPLIT
+#define MSD_SPLIT 1                    // 2: all 16 pass-1 warps on every item, two per region
+#endif
+constexpr int NSPLIT = MSD_SPLIT;      // pass-1 warps per region of an item
+constexpr int NG1 = 2 / NSPLIT;        // pass-1 warp groups: group g processes items j = g mod NG1
+constexpr int NW1 = NCW * NSPLIT;      // pass-1 warps per item
+constexpr int CORE_THREADS = (W_P1 + NG1 * NW1) * 32;
 static_assert(W_RED < W_P2 && W_P2 % 4 == 0 && W_P1 % 4 == 0 && NCW % NCW2 == 0 && NCW2 % 4 == 0, "warp roles");
 constexpr int SMAX = 14;               // ring stages (upper bound)
 constexpr int NQ = 16;                 // per-item record slots (references, pass-2 factors)
@@ -95,12 +100,12 @@ struct Ctl {
     uint64_t pub[NQ];                       // this CTA's slice record of item j is published
     uint32_t p1cnt[R1];                     // pass-1 warps done with the item of a record slot
     uint32_t taddr;
-    float wmx[NQ][L][NCW];                  // per-warp max of each row, per item
+    float wmx[NQ][L][NW1];                  // per-warp max of each row, per item
     uint32_t clampw[NQ];                    // bit w: pass-1 warp w took the clamped path
-    alignas(16) float r1S[R1][L][NCW][NSUB1];  // pass-1 partial sums
-    alignas(16) float r1K[R1][L][NCW][NSUB1];  // pass-1 KL numerators sum e (z_l - z_{l-1})
-    int r1A[R1][L][NCW];                    // greedy: first argmax index per warp
-    WF rowf[NQ][L][NCW];
+    alignas(16) float r1S[R1][L][NW1][NSUB1];  // pass-1 partial sums
+    alignas(16) float r1K[R1][L][NW1][NSUB1];  // pass-1 KL numerators sum e (z_l - z_{l-1})
+    int r1A[R1][L][NW1];                    // greedy: first argmax index per warp
+    WF rowf[NQ][L][NW1];
     float r2R[R2][L][NCW2][NSUB];           // pass-2 residual partials (probability units)
     unsigned long long fbuf_pad;
     unsigned long long fbuf[NFETCH][FBUF];  // fetcher staging of a unit's records
@@ -250,12 +255,12 @@ __device__ __noinline__ uint4 load_straddle(const Tin* sl, const Tin* g, int e0,
 // the pass-1 loads stay unconditional.  Out of line.
 template <typename Tin, int L, int NV>
 __device__ __noinline__ void repair_stage(Tin* stage, int rs, const LevelDesc& lv, int64_t b, int64_t i,
-                                          int64_t base, int w, int lane, int len_bulk, int len) {
+                                          int64_t base, int w, int lane, int len_bulk, int len, int jv0, int jv1) {
     constexpr int VEC = Elem<Tin>::VEC;
     const int hoff = (w / HREG) * VS;            // this region's half of the ring row
     for (int l = 0; l < L; ++l) {
         Tin* sl = stage + (size_t)l * rs + hoff;
-        for (int jv = 0; jv < NV; ++jv) {
+        for (int jv = jv0; jv < jv1; ++jv) {
             const int e0 = vec_index<Tin>(w, lane, jv) - hoff;
             if (e0 + VEC <= len_bulk || e0 >= len) continue;
             const uint4 v = load_straddle<Tin>(
@@ -461,15 +466,17 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     if (warp == W_PROD) {
         if (lane == 0) {
             // empty: one arrival per region (pass-1 warps for T items, pass-2 warps for R items)
-            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], nact); }
-            for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], nact); mbar_init(&c.r1_empty[r], 1); }
+            // a T item's stage is released by its NSPLIT * nact pass-1 warps, an R item's by the
+            // nact pass-2 warps (NSPLIT arrivals each)
+            for (int s = 0; s < S; ++s) { mbar_init(&c.full[s], 1); mbar_init(&c.empty[s], nact * NSPLIT); }
+            for (int r = 0; r < R1; ++r) { mbar_init(&c.r1_full[r], nact * NSPLIT); mbar_init(&c.r1_empty[r], 1); }
             for (int r = 0; r < R2; ++r) { mbar_init(&c.r2_full[r], np2); mbar_init(&c.r2_empty[r], 1); }
             for (int k = 0; k < NQ; ++k) {
                 mbar_init(&c.rowf_full[k], 1);
                 mbar_init(&c.rowf_empty[k], np2);
                 mbar_init(&c.pub[k], 1);
             }
-            for (int q = 0; q < NT; ++q) { mbar_init(&c.tm_full[q], nact); mbar_init(&c.tm_empty[q], np2); }
+            for (int q = 0; q < NT; ++q) { mbar_init(&c.tm_full[q], nact * NSPLIT); mbar_init(&c.tm_empty[q], np2); }
             fence_mbar_init();
         }
         __syncwarp();
@@ -516,16 +523,28 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         item(j, u, b, i);
         const int k = j & (NQ - 1);
         const int r1 = j & (R1 - 1);
-        float Sw = 0.f, Kw = 0.f, wm = -INFINITY;
-        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        int aw = 0x7fffffff;
-        if (act) {
-            s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][w][0]);
-            const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][w][0]);
-            Sw = (s4.x + s4.y) + (s4.z + s4.w);
-            Kw = (k4.x + k4.y) + (k4.z + k4.w);
-            wm = c.wmx[k][l][w];
-            if (GREEDY) aw = c.r1A[r1][l][w];
+        // the NSPLIT pass-1 warps of region w (each with its own warp maximum)
+        float Sh[NSPLIT], Kh[NSPLIT], wmh[NSPLIT];
+        double Sdh[NSPLIT];
+        int ah[NSPLIT];
+        float wm = -INFINITY;
+#pragma unroll
+        for (int h = 0; h < NSPLIT; ++h) {
+            Sh[h] = Kh[h] = 0.f;
+            Sdh[h] = 0.0;
+            wmh[h] = -INFINITY;
+            ah[h] = 0x7fffffff;
+            if (act) {
+                const int wq = w + NCW * h;
+                const float4 s4 = *reinterpret_cast<const float4*>(&c.r1S[r1][l][wq][0]);
+                const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][wq][0]);
+                Sh[h] = (s4.x + s4.y) + (s4.z + s4.w);
+                Sdh[h] = ((double)s4.x + (double)s4.y) + ((double)s4.z + (double)s4.w);
+                Kh[h] = (k4.x + k4.y) + (k4.z + k4.w);
+                wmh[h] = c.wmx[k][l][wq];
+                if (GREEDY) ah[h] = c.r1A[r1][l][wq];
+                wm = max_nan_f32(wm, wmh[h]);
+            }
         }
         __syncwarp();
         if (lane == 0) {
@@ -536,11 +555,19 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         float msl = wm;
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
-        float f = wm == msl ? 1.f : ex2f((wm - msl) * l2s);
-        if (!(wm > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked region
-        // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
-        float Sx = Sw * f, Kx = (l > 0 && f != 0.f) ? f * Kw : 0.f;
-        int ax = (wm == msl) ? aw : 0x7fffffff;
+        // each warp's records scaled to the slice maximum (factor 1 when the warp holds it)
+        float Sx = 0.f, Kx = 0.f, fh[NSPLIT];
+        int ax = 0x7fffffff;
+#pragma unroll
+        for (int h = 0; h < NSPLIT; ++h) {
+            float f = wmh[h] == msl ? 1.f : ex2f((wmh[h] - msl) * l2s);
+            if (!(wmh[h] > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked warp region
+            fh[h] = f;
+            Sx += Sh[h] * f;
+            // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
+            if (l > 0 && f != 0.f) Kx += f * Kh[h];
+            if (wmh[h] == msl) ax = min(ax, ah[h]);
+        }
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) {
             Sx += __shfl_xor_sync(0xffffffffu, Sx, o);
@@ -566,7 +593,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // float64 from the sub-records (the row normalisers' precision decides the KL and
         // acceptance errors of the tail), the KL numerator in fp32
         // (hardware float -> double conversions: off the latency path, few instructions)
-        double Sd = (((double)s4.x + (double)s4.y) + ((double)s4.z + (double)s4.w)) * (double)f;
+        double Sd = 0.0;
+#pragma unroll
+        for (int h = 0; h < NSPLIT; ++h) Sd += Sdh[h] * (double)fh[h];
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) {
             Sd += __shfl_xor_sync(0xffffffffu, Sd, o);
@@ -597,8 +626,12 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // waits overlap the other group's exponentials.  Reference: the warp maximum of the
         // row (the dominant entries then have |z - m| small, so the fp32 exponent argument
         // keeps full relative accuracy).  Rows are processed in two 8-element halves.
-        const int g1 = (warp - W_P1) / NCW;
-        const int rg = (warp - W_P1) % NCW;     // element region
+        const int g1 = (warp - W_P1) / NW1;
+        const int wi = (warp - W_P1) % NW1;     // warp of the item (record index)
+        const int rg = wi % NCW;                // element region
+        const int hs = wi / NCW;                // split of the region: vectors / quarters of this warp
+        constexpr int QPW = (CET / 8) / NSPLIT; // 8-element quarters per warp and row
+        constexpr int VPW = NV / NSPLIT;        // vectors per warp and row
         const int hh = rg / HREG;               // its half (tail slice NH s + hh)
         const int gofs = (int)hbase[hh] - hh * VS;   // ring-row index -> vocabulary id
         if ((amask >> rg) & 1u) {
@@ -623,17 +656,18 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     continue;
                 }
                 PROF(0)
-                if (rg == 0 && lane == 0) stamp(j, 1);
+                if (wi == 0 && lane == 0) stamp(j, 1);
                 // a row length that is not a multiple of 16 bytes: patch the straddling vector
                 if (hbulk[hh] != hlen[hh])
-                    repair_stage<Tin, L, NV>(stage, RS, p.lv, b, i, hbase[hh], rg, lane, hbulk[hh], hlen[hh]);
+                    repair_stage<Tin, L, NV>(stage, RS, p.lv, b, i, hbase[hh], rg, lane, hbulk[hh], hlen[hh],
+                                             hs * VPW, (hs + 1) * VPW);
                 // per-thread then per-warp max of every row (NaN-propagating)
                 float wm[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
                     float tm = -INFINITY;
 #pragma unroll
-                    for (int jv = 0; jv < NV; ++jv) {
+                    for (int jv = hs * VPW; jv < (hs + 1) * VPW; ++jv) {
                         const uint4 r = *reinterpret_cast<const uint4*>(stage + (size_t)l * RS + vec_index<Tin>(rg, lane, jv));
                         if (ES == 2) {
                             const uint32_t mx = max_nan_bf16x2(max_nan_bf16x2(r.x, r.y), max_nan_bf16x2(r.z, r.w));
@@ -653,7 +687,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
                 if (j >= R1 && !p1only) mbar_wait(&c.r1_empty[r1], (uint32_t)(((j / R1) - 1) & 1));
-                if (rg == 0 && lane == 0) stamp(j, 2);
+                if (wi == 0 && lane == 0) stamp(j, 2);
                 PROF(1)
                 float Sv[L], Kv[L];
                 int am[L];
@@ -667,7 +701,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         am[l] = 0x7fffffff;
                     }
 #pragma unroll
-                    for (int h = 0; h < CET / 8; ++h) {
+                    for (int h = hs * QPW; h < (hs + 1) * QPW; ++h) {
                         float2 yprev[4];
 #pragma unroll
                         for (int l = 0; l < L; ++l) {
@@ -727,7 +761,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     for (int l = 0; l < L; ++l) {
                         float tm = -INFINITY;
 #pragma unroll
-                        for (int jv = 0; jv < NV; ++jv) {
+                        for (int jv = hs * VPW; jv < (hs + 1) * VPW; ++jv) {
                             float xs[VEC];
                             unpack_clamped<Tin>(*reinterpret_cast<const uint4*>(stage + (size_t)l * RS + vec_index<Tin>(rg, lane, jv)), xs);
 #pragma unroll
@@ -753,8 +787,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 if (lane == 0) {
                     if (isT || p1only) mbar_arrive(&c.empty[cu.st]);
 #pragma unroll
-                    for (int l = 0; l < L; ++l) c.wmx[k][l][rg] = wm[l];
-                    const uint32_t bit = 1u << rg;
+                    for (int l = 0; l < L; ++l) c.wmx[k][l][wi] = wm[l];
+                    const uint32_t bit = 1u << wi;
                     if (fast) atomicAnd(&c.clampw[k], ~bit);
                     else atomicOr(&c.clampw[k], bit);
                 }
@@ -762,12 +796,12 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 if (lane < NSUB1) {
 #pragma unroll
                     for (int l = 0; l < L; ++l) {
-                        c.r1S[r1][l][rg][lane] = Sv[l];
-                        c.r1K[r1][l][rg][lane] = Kv[l];
+                        c.r1S[r1][l][wi][lane] = Sv[l];
+                        c.r1K[r1][l][wi][lane] = Kv[l];
                     }
                     if (GREEDY && lane == 0) {
 #pragma unroll
-                        for (int l = 0; l < L; ++l) c.r1A[r1][l][rg] = am[l];
+                        for (int l = 0; l < L; ++l) c.r1A[r1][l][wi] = am[l];
                     }
                 }
                 PROF(4)
@@ -776,7 +810,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 }
                 __syncwarp();
-                if (rg == 0 && lane == 0) stamp(j, 3);
+                if (wi == 0 && lane == 0) stamp(j, 3);
 #if defined(MSD_TRACE) && !defined(MSD_PROF)
                 if (lane == 0 && p.trace)
                     atomicMax(p.trace + ((int64_t)(grp + j * kgrp) * Cc + sfix) * 16 + 7, (unsigned long long)globaltimer());
@@ -822,13 +856,17 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const int r2 = j & (R2 - 1);
                 mbar_wait_lat(&c.rowf_full[k], (uint32_t)((j / NQ) & 1));
                 PROF(0)
-                float rh[L], sc[L], wm[L];
+                // factors of the region's NSPLIT pass-1 warps (chunk ch belongs to split ch NSPLIT / 2)
+                float rh[L][NSPLIT], sc[L][NSPLIT], wm[L][NSPLIT];
                 const uint32_t cw = c.clampw[k];
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
-                    rh[l] = l > 0 ? c.rowf[k][l][v].rho : 0.f;
-                    sc[l] = l > 0 ? c.rowf[k][l][v].scale : 0.f;
-                    wm[l] = c.wmx[k][l][v];
+#pragma unroll
+                    for (int h = 0; h < NSPLIT; ++h) {
+                        rh[l][h] = l > 0 ? c.rowf[k][l][v + NCW * h].rho : 0.f;
+                        sc[l][h] = l > 0 ? c.rowf[k][l][v + NCW * h].scale : 0.f;
+                        wm[l][h] = c.wmx[k][l][v + NCW * h];
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&c.rowf_empty[k]);
@@ -839,8 +877,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 float2 a2[L];
 #pragma unroll
                 for (int l = 0; l < L; ++l) a2[l] = make_float2(0.f, 0.f);
-                auto pair = [&](int l, const float* ea, const float* eb) {
-                    const float2 nr = make_float2(-rh[l], -rh[l]);
+                auto pair = [&](int l, int hc, const float* ea, const float* eb) {
+                    const float2 nr = make_float2(-rh[l][hc], -rh[l][hc]);
                     float2 x = make_float2(0.f, 0.f), xb = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int kk = 0; kk < CH; kk += 2) {
@@ -850,7 +888,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         if (kk & 2) xb = __fadd2_rn(xb, t);
                         else x = __fadd2_rn(x, t);
                     }
-                    a2[l] = __fadd2_rn(a2[l], __fadd2_rn(x, xb));
+                    const float2 xs = __fadd2_rn(x, xb);
+                    a2[l] = __ffma2_rn(xs, make_float2(sc[l][hc], sc[l][hc]), a2[l]);
                 };
                 if (isT) {
                     mbar_wait_lat(&c.tm_full[q], (uint32_t)cu.tph);
@@ -860,20 +899,21 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const uint32_t tb = tcol(v) + (uint32_t)(q * CET * L);
 #pragma unroll
                     for (int ch = 0; ch < CET / CH; ++ch) {
+                        const int hc = ch * NSPLIT / (CET / CH);
                         float ea[CH], eb[CH], ec[CH];
                         tm_ld16(tb + (uint32_t)(ch * CH), eb);
                         tm_ld16(tb + (uint32_t)(CET + ch * CH), ea);
                         if (L > 2) tm_ld16(tb + (uint32_t)(2 * CET + ch * CH), ec);
                         tm_wait_ld();
-                        pair(1, ea, eb);
-                        if (L > 2) pair(2, ec, ea);
+                        pair(1, hc, ea, eb);
+                        if (L > 2) pair(2, hc, ec, ea);
 #pragma unroll
                         for (int l = 3; l < L; ++l) {
 #pragma unroll
                             for (int kk = 0; kk < CH; ++kk) eb[kk] = ec[kk];
                             tm_ld16(tb + (uint32_t)(l * CET + ch * CH), ec);
                             tm_wait_ld();
-                            pair(l, ec, eb);
+                            pair(l, hc, ec, eb);
                         }
                     }
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -889,10 +929,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const Tin* stage = ring + (size_t)cu.st * L * RS;
                     const bool skip_r = (p.dbg & 2) != 0;   // debug: R items skip the recomputation
                     if (!skip_r) {
-                        const bool clamp = ((cw >> v) & 1u) || ES == 4;
                         constexpr int NVC = CH / VEC;      // vectors per chunk
 #pragma unroll
                         for (int ch = 0; ch < CET / CH; ++ch) {
+                            const int hc = ch * NSPLIT / (CET / CH);
+                            const bool clamp = ((cw >> (v + NCW * hc)) & 1u) || ES == 4;
                             float eprev[CH];
 #pragma unroll
                             for (int l = 0; l < L; ++l) {
@@ -903,19 +944,19 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                                                                               vec_index<Tin>(v, lane, ch * NVC + jv));
                                 float e[CH];
                                 float2 y[CH / 2];
-                                row_exp<Tin>(raw, wm[l], clamp, e, y, l2s);
-                                if (l > 0) pair(l, e, eprev);
+                                row_exp<Tin>(raw, wm[l][hc], clamp, e, y, l2s);
+                                if (l > 0) pair(l, hc, e, eprev);
 #pragma unroll
                                 for (int kk = 0; kk < CH; ++kk) eprev[kk] = e[kk];
                             }
                         }
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&c.empty[cu.st]);
+                    if (lane == 0) mbar_arrive_cnt(&c.empty[cu.st], (uint32_t)NSPLIT);
                     PROF(2)
                 }
 #pragma unroll
-                for (int l = 1; l < L; ++l) acc[l] = (a2[l].x + a2[l].y) * sc[l];
+                for (int l = 1; l < L; ++l) acc[l] = a2[l].x + a2[l].y;
 #pragma unroll
                 for (int l = 1; l < L; ++l) acc[l] = fold4(acc[l]);
                 PROF(3)
@@ -1087,10 +1128,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             PROF(1)
             if (j >= NQ) mbar_wait(&c.rowf_empty[k], (uint32_t)(((j / NQ) - 1) & 1));
             PROF(2)
-            // per-region factors: x = NCW (l - 1) + w for region w and the pair ending at row l
-            for (int x = lane; x < (L - 1) * NCW; x += 32) {
-                const int w = x % NCW, l = 1 + x / NCW;
-                if ((amask >> w) & 1u) {
+            // per pass-1-warp factors: x = NW1 (l - 1) + w for warp w and the pair ending at row l
+            for (int x = lane; x < (L - 1) * NW1; x += 32) {
+                const int w = x % NW1, l = 1 + x / NW1;
+                if ((amask >> (w % NCW)) & 1u) {
                     float Ma = Rl[0], Mb = Rl[0], Sa = Sl[0], Sb = Sl[0];
 #pragma unroll
                     for (int r = 1; r < L; ++r)
