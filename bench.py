@@ -465,6 +465,7 @@ def run_ours(args):
                        "kv": "paged, 16-token blocks, seq_len U[512,4096], reset each step"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "msd_core",
+                         "frac_of_nominal_8tbs": achieved / 8000.0,
                          "algorithmic_bytes_per_launch": core_bytes,
                          "core_ms_per_launch": core_avg_ms,
                          "core_share_of_step": core_avg_ms / ms,
