@@ -322,7 +322,8 @@ msd_status msd_debug_set_trace(void* dev_buf, size_t bytes);
 /* msd_debug_set_knobs: process-wide test / diagnostic overrides of internal choices (the library
  * reads no environment variables).  pat_t / pat_r: core item pattern (TMEM-parked items, ring-
  * kept items per period; -1 = default); stages: TMA ring depth (-1 = default); core_dbg: core
- * isolation mode (0 = normal; 1 = pass 1 + ring only, results invalid; 4|1 = ring only);
+ * isolation mode (0 = normal; 1 = pass 1 + ring only, results invalid; 4|1 = ring only; bits
+ * 8..11 = L2 prefetch distance in items + 1, 0 = the default 2);
  * exact_draws: 1 = every residual / bonus draw takes the float64 exact path; z_safe: residual
  * mass below which a draw takes the exact path (default 0.05, R4; < 0 = default).
  * The outputs are identical for every pattern / stage choice and for exact_draws 0 / 1 outside

@@ -89,7 +89,7 @@ struct ExactJob {
     uint32_t pad[5];
 };
 struct JobBoard {
-    uint32_t alloc, started, finished, pad0;
+    uint32_t alloc, started, finished, next;   // next: the tail's request counter (persistent grid)
     ExactJob job[EXJ_MAX];
     double part1[EXJ_MAX][EXJ_NCH][2];
     double part2[EXJ_MAX][EXJ_MAXS];
@@ -199,6 +199,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "%2, [%3], %4;" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
+}
+// fire-and-forget request of [src, src + bytes) into L2 (no shared memory, no barrier)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;

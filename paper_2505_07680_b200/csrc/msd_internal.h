@@ -29,6 +29,7 @@ struct CoreParams {
     int32_t stages;     // TMA ring stages (host-computed from the shared-memory budget)
     int32_t rs;         // ring row stride in entries (active pass-1 warps x 512)
     int32_t pat_p, pat_t;   // item pattern: of every pat_p items the first pat_t park e in TMEM
+    int32_t pf_dist;        // items requested into L2 ahead of their ring copies (0: none)
     Partial* partials;
     float2* partms;     // compact (slice max, slice sum) for the pass-2 exchange
     RowStat* rowstat;
