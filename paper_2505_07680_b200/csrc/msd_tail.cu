@@ -64,6 +64,8 @@ struct TailShared {
     int32_t sel_slice;
     int32_t ex_job, ex_ok, ex_go, ex_pick, ex_phase, ex_chunk;   // exact-draw job board scratch
     float zpre[MAXL][MAXC];       // z_l[b, i, x_i]: the draft token's logit in every row i < K
+    float ua[MAXL][MAXC], ue[MAXL][MAXC];   // the request's acceptance / emission uniforms
+    int32_t ftok, fclear;         // fast-path draw: crossing token, decided outside the margins
     const double* exptab;         // exp of every bf16 value (float64), or NULL
 };
 constexpr size_t TAIL_DYN_MAX = 96 * 1024;   // prefetched partials + slice residuals
@@ -478,6 +480,60 @@ __device__ __forceinline__ int scan_find(WF w, int64_t e0, double before, double
     return block_min_i(*found, sh);
 }
 
+// Fast-pass inverse-CDF step in float32, relative to the slice: thread t holds the ET weights of
+// entries [e0, e0 + ET); `t` is the slice-local target (target - before) and `margin` the
+// decision margin.  Every thread's exclusive / inclusive prefix is formed with the same
+// operations as its neighbours' (warp scan, then the preceding warps' totals summed in a fixed
+// order), so exactly one thread holds a crossing; it scans its weights and records the token and
+// whether the crossing lies farther than `margin` from both of its boundaries.  Two barriers.
+// The float32 accumulation error (< 30 roundings of the slice mass, ~2e-6 Z) is far inside the
+// margin (2e-5 Z).  Returns the token or 0x7fffffff (none: the caller takes the float64 pass).
+__device__ __forceinline__ int scan_find_f32(const float* w, int64_t e0, float t, float margin, TailShared& sh,
+                                             bool* clear) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float q[ET / 2];
+#pragma unroll
+    for (int k = 0; k < ET / 2; ++k) q[k] = w[2 * k] + w[2 * k + 1];
+#pragma unroll
+    for (int h = ET / 4; h > 0; h >>= 1)
+#pragma unroll
+        for (int k = 0; k < h; ++k) q[k] = q[k] + q[k + h];
+    const float loc = q[0];
+    float incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl = 0.f;
+    if (threadIdx.x == 0) { sh.ftok = 0x7fffffff; sh.fclear = 0; }
+    if (lane == 31) sh.red_f[warp] = incl;
+    __syncthreads();
+    float woff = 0.f;
+#pragma unroll
+    for (int wi = 0; wi < NWARP - 1; ++wi)
+        if (wi < warp) woff += sh.red_f[wi];
+    const float lo = woff + excl, hi = woff + incl;
+    if (loc > 0.f && lo <= t && t < hi) {
+        float c = lo, cp = lo;
+        int kk = -1;
+#pragma unroll
+        for (int k = 0; k < ET; ++k) {
+            const float c0 = c;
+            c += w[k];
+            if (kk < 0 && w[k] > 0.f && c > t) { kk = k; cp = c0; }
+        }
+        if (kk >= 0) {
+            sh.ftok = (int)(e0 + kk);
+            sh.fclear = (t - cp > margin && (c - t) > margin) ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    *clear = sh.fclear != 0;
+    return sh.ftok;
+}
+
 // Inverse-CDF search inside slice s with weights wt(), given the float64 mass of all earlier
 // slices (`before`) and the target u*Z.  Thread t scans the 16 contiguous entries
 // [t*16, t*16+16) of the slice.  Returns the token or -1.
@@ -492,6 +548,9 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
     const int64_t e0 = (int64_t)s * vse + threadIdx.x * ET;
     V = min(V, (int64_t)(s + 1) * vse);
     if (threadIdx.x == 0) { sh.near = 0; sh.found = 0; }
+#ifdef MSD_PROF
+    long long q0 = clock64();
+#endif
     float xa[ET], xb[ET];
     load16<Tin>(ra, e0, V, xa);
     if (resid) load16<Tin>(rb, e0, V, xb);
@@ -513,14 +572,22 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
             }
             wf[k] = wk;
         }
-        const int best = scan_find([&](int k) { return wf[k]; }, e0, before, target, sh, &found, &cprev_f, &c_f);
-        if (best != 0x7fffffff && found == best)
-            sh.found = (fabs(target - cprev_f) < DRAW_MARGIN_REL * Z + DRAW_MARGIN_ABS ||
-                        fabs(c_f - target) < DRAW_MARGIN_REL * Z + DRAW_MARGIN_ABS) ? 1 : 0;
-        __syncthreads();
-        const bool clear = best != 0x7fffffff && sh.found == 0;
-        __syncthreads();
-        if (clear) {
+#ifdef MSD_PROF
+        if (threadIdx.x == 0) { const long long q = clock64(); atomicAdd(&g_tail_prof[9], (unsigned long long)(q - q0)); q0 = q; }
+#endif
+        // c - t and t - cp are slice-local float32 distances; the crossing token's own boundaries
+        bool clear;
+        const int best = scan_find_f32(wf, e0, (float)(target - before), (float)(DRAW_MARGIN_REL * Z + DRAW_MARGIN_ABS),
+                                       sh, &clear);
+#ifdef MSD_PROF
+        if (threadIdx.x == 0) {
+            const long long q = clock64();
+            atomicAdd(&g_tail_prof[10], (unsigned long long)(q - q0));
+            atomicAdd(&g_tail_prof[15], 1ull);
+            if (!clear) atomicAdd(&g_tail_prof[14], 1ull);
+        }
+#endif
+        if (best != 0x7fffffff && clear) {
             *tie = false;
             return best;
         }
@@ -967,6 +1034,15 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
         const int32_t x = p.cand0[b * K + i];
         sh.zpre[l][i] = (x >= 0 && x < V) ? clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l, b, i) + x)) : NEG_CLAMP;
     }
+    // the request's uniforms, in the same round trip (acceptance and emission read them later)
+    if (!p.greedy) {
+        const int W = K + L - 1;
+        for (int t = tid; t < (L - 1) * W; t += T) {
+            const int l = t / W, i = t % W;
+            sh.ua[l][i] = p.u_acc[l * p.ua_l + b * p.ua_b + i];
+            sh.ue[l][i] = p.u_emit[l * p.ue_l + b * p.ue_b + i];
+        }
+    }
     __syncthreads();
     TPROF(12)
     // row normalisers (Eq. 1) and KL numerators of every draft-position row, combined from
@@ -1028,7 +1104,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
                     const bool draft = i < K && t == p.cand0[b * K + i];
                     const float za = draft ? sh.zpre[l][i] : clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l, b, i) + t));
                     const float zb = draft ? sh.zpre[l - 1][i] : clamp1(Elem<Tin>::load1(row_ptr<Tin>(p, l - 1, b, i) + t));
-                    const double u = (double)p.u_acc[(l - 1) * p.ua_l + b * p.ua_b + i];
+                    const double u = (double)sh.ua[l - 1][i];
                     if (!(za > NEG_MASKED)) {
                         acc = false;
                         tie = u < TIE_EPS;
@@ -1107,7 +1183,7 @@ __global__ void __launch_bounds__(T, MSD_TAIL_MINB) tail_kernel(TailParams p) {
             if (p.greedy) {
                 y = A.amax;
             } else {
-                const double u = (double)p.u_emit[(l - 1) * p.ue_l + b * p.ue_b + pos];
+                const double u = (double)sh.ue[l - 1][pos];
                 // per-slice weights
                 if (resid) {
                     if (pos < K) {

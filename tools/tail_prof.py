@@ -20,6 +20,7 @@ lib.msd_debug_tail_prof(buf, 1)
 names = ["combine rows", "extra rows", "acceptance", "dtv/kl", "emission(rest)", "next cands", "outputs", "emit: weights", "emit: draw_slices"]
 B = c["B"]
 print(f"{name}: tail cycles per request (thread 0): " + "  ".join(f"{n} {buf[k] / B:.0f}" for k, n in enumerate(names)))
+print(f"fast-path slice scans {buf[15]}, of which undecided (float64 rescan) {buf[14]}; cycles per scan: loads+weights {buf[9] / max(buf[15], 1):.0f} scan_find {buf[10] / max(buf[15], 1):.0f} decision {buf[11] / max(buf[15], 1):.0f}")
 fl = cv.flags.cpu()
 print("requests with EXACT_DRAW:", int(((fl & api.FLAG['EXACT_DRAW']) != 0).sum()), " RESID_SMALL:", int(((fl & api.FLAG['RESID_SMALL']) != 0).sum()))
 print("n_acc mean per level:", cv.n_acc.float().mean(1).tolist(), " m_cand mean:", cv.m_cand.float().mean(1).tolist())
