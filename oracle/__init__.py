@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
         L.or_pool_divergence.argtypes = [P, i32, i32, i32, i64, P, P]
         L.or_draft_sample.restype = None
         L.or_draft_sample.argtypes = [P, i64, i32, i64, P, i32, d, P, P, P, P]
+        L.or_logits_threshold.restype = d
+        L.or_logits_threshold.argtypes = [P, i64, d, i32, d, d, P]
         _ = u32
         _lib = L
     return _lib
@@ -295,3 +297,28 @@ def draft_sample(z, u, greedy=False, tie_eps_draw=1e-7):
     lib().or_draft_sample(_p(z), V, B, V, _p(u), int(bool(greedy)), tie_eps_draw,
                           _p(out["token"]), _p(out["lse"]), _p(out["q_tok"]), _p(out["near_tie"]))
     return out
+
+
+def logits_threshold(z, temperature=1.0, top_k=0, top_p=1.0, eps=1e-6):
+    """top-k / top-p threshold of one logit row (R19 / R23):
+    returns (tau, near): entries z < tau are removed (ties at tau kept); NaN for NaN / +inf rows."""
+    z = _f64(z).ravel()
+    near = np.zeros(1, np.int32)
+    tau = lib().or_logits_threshold(_p(z), z.size, float(temperature), int(top_k), float(top_p),
+                                    float(eps), _p(near))
+    return float(tau), int(near[0])
+
+
+def logits_process(z, temperature=1.0, top_k=0, top_p=1.0, eps=1e-6):
+    """Row-wise top-k / top-p over z [..., V] (float64 copy): removed entries are -inf; rows with
+    NaN / +inf are returned unchanged.  Returns (z_processed, tau [...], near [...])."""
+    z = _f64(z)
+    flat = z.reshape(-1, z.shape[-1])
+    out = flat.copy()
+    tau = np.zeros(flat.shape[0])
+    near = np.zeros(flat.shape[0], np.int32)
+    for r in range(flat.shape[0]):
+        tau[r], near[r] = logits_threshold(flat[r], temperature, top_k, top_p, eps)
+        if not np.isnan(tau[r]):
+            out[r][flat[r] < tau[r]] = -np.inf
+    return out.reshape(z.shape), tau.reshape(z.shape[:-1]), near.reshape(z.shape[:-1])

@@ -520,3 +520,52 @@ void or_draft_sample(const double* z, int64_t ld, int32_t B, int64_t V, const fl
         near_tie[b] = nt;
     }
 }
+
+/* Logits processors top-k / top-p ("sets up sampling parameters
+ * (LogitsProcessorList)"; R19 / R23).  The paper names the processor list only; the
+ * reading is Hugging Face's TemperatureLogitsWarper -> TopKLogitsWarper -> TopPLogitsWarper order
+ * with whole tie groups kept: sort the row's values in descending order;
+ *   top-k (0 < k < V): tau_k = the k-th largest value (every entry equal to it is kept);
+ *   top-p (0 < p < 1): over softmax(z / T) restricted to the entries z >= tau_k, walk the groups of
+ *     equal values from the largest; tau_p = the value of the first group at which the cumulative
+ *     mass reaches p * Z (Z = the kept mass), i.e. the smallest top set of mass >= p;
+ *   tau = max(tau_k, tau_p); entries z < tau are removed (-inf).  Off: tau = -inf.
+ * near = the cumulative mass before or after the chosen group lies within eps * Z of p * Z (the
+ * decision is a floating-point tie).  A row holding a NaN or +inf returns NaN (not processed). */
+static int cmp_desc(const void* a, const void* b) {
+    const double x = *(const double*)a, y = *(const double*)b;
+    return (x < y) - (x > y);
+}
+double or_logits_threshold(const double* z, int64_t V, double T, int32_t top_k, double top_p,
+                           double eps, int32_t* near) {
+    *near = 0;
+    double* s = (double*)malloc(sizeof(double) * (size_t)V);
+    for (int64_t v = 0; v < V; ++v) {
+        if (isnan(z[v]) || z[v] == INFINITY) { free(s); return NAN; }
+        s[v] = z[v];
+    }
+    qsort(s, (size_t)V, sizeof(double), cmp_desc);
+    double tau_k = -INFINITY, tau_p = -INFINITY;
+    if (top_k > 0 && top_k < V) tau_k = s[top_k - 1];
+    if (top_p > 0.0 && top_p < 1.0 && s[0] > -INFINITY) {
+        const double M = s[0];
+        double Z = 0.0;
+        for (int64_t v = 0; v < V && s[v] >= tau_k; ++v) Z += exp((s[v] - M) / T);
+        const double target = top_p * Z;
+        double cum = 0.0;
+        for (int64_t v = 0; v < V && s[v] >= tau_k;) {
+            int64_t e = v;
+            while (e < V && s[e] == s[v]) ++e;          /* group of equal values [v, e) */
+            const double before = cum;
+            cum += (double)(e - v) * exp((s[v] - M) / T);
+            if (cum >= target) {
+                tau_p = s[v];
+                *near = (fabs(cum - target) < eps * Z || fabs(before - target) < eps * Z) ? 1 : 0;
+                break;
+            }
+            v = e;
+        }
+    }
+    free(s);
+    return tau_k > tau_p ? tau_k : tau_p;
+}

@@ -111,6 +111,13 @@ void or_draft_sample(const double* z, int64_t ld, int32_t B, int64_t V, const fl
                      int32_t greedy, double tie_eps_draw, int32_t* token, double* lse,
                      double* q_tok, int32_t* near_tie);
 
+/* Logits processors top-k / top-p (R19 / R23): the row's
+ * threshold tau (entries z < tau are removed; ties at tau kept), NaN for a row holding NaN / +inf;
+ * near = the top-p boundary decision lies within eps * Z of p * Z.  Pinned by
+ * tests/test_oracle_proc.py (brute-force subsets, Hugging Face's warpers, closed forms). */
+double or_logits_threshold(const double* z, int64_t V, double T, int32_t top_k, double top_p,
+                           double eps, int32_t* near);
+
 #ifdef __cplusplus
 }
 #endif
