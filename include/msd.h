@@ -169,13 +169,14 @@ size_t msd_chain_verify_workspace(int32_t L, int32_t B, int32_t K, int64_t V);
  * temperature-scaled distributions; greedy mode is unchanged (argmax z / T = argmax z).  The
  * logits are read once as before (the scale is applied inside the kernels, never written back).
  * proc (host pointer, NULL = msd_chain_verify): temperature in (1e-6, 1e6]; top_k must be 0 and
- * top_p 1 (or <= 0): top-k / top-p need a per-row threshold before the normaliser and are not
- * implemented (MSD_E_ARG).  All other arguments as msd_chain_verify.
+ * top_p 1 (or <= 0) here (MSD_E_ARG otherwise): top-k / top-p are applied beforehand by
+ * msd_logits_process on every level (they remove entries; the temperature stays fused here).  All
+ * other arguments as msd_chain_verify.
  * ------------------------------------------------------------------------- */
 typedef struct {
     float temperature;   /* T > 0; 1 = no scaling */
-    int32_t top_k;       /* 0 = off (only value accepted) */
-    float top_p;         /* 1 = off (only value accepted; <= 0 also means off) */
+    int32_t top_k;       /* 0 = off (msd_chain_verify_proc: only value accepted) */
+    float top_p;         /* 1 = off (<= 0 also means off; msd_chain_verify_proc: only value accepted) */
 } msd_processors;
 msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
                                  const int32_t* draft_tok, const float* u_acc, const float* u_emit,
@@ -284,6 +285,30 @@ msd_status msd_pool_divergence(const msd_logits* models, int32_t N, int32_t B, i
 msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, int64_t V,
                             const float* u, int32_t greedy, int32_t* token, float* lse,
                             float* q_tok, uint32_t* flags, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * msd_logits_process -- top-k / top-p logits processors ("sets up
+ *    sampling parameters (LogitsProcessorList)"; R19 / R23: Hugging Face's
+ *    Temperature -> TopK -> TopP warper order, whole tie groups kept).  Per row of one level:
+ *    tau_k = the top_k-th largest logit (0 < top_k < V; else -inf); over softmax(z / T) of the
+ *    entries z >= tau_k, tau_p = the value at which the cumulative mass of the groups of equal
+ *    values, largest first, reaches top_p (0 < top_p < 1; else -inf); tau = max(tau_k, tau_p).
+ *    out = z where z >= tau, -inf elsewhere.  Call once per chain level, then
+ *    msd_chain_verify_proc with the same temperature (top_k 0, top_p 1) on the outputs.
+ * in, out (HOST pointers to one descriptor each; same dtype; out->ptr may equal in->ptr: in
+ *    place): rows [0, rows) of every request b < B are processed; V <= ld; 16-byte aligned rows.
+ * proc: temperature (the top-p masses), top_k >= 0, top_p.
+ * tau[B][rows] (device f32, NULL ok): the threshold (-inf when nothing is removed; NaN for a row
+ *    holding NaN or +inf, which is passed through unchanged and flagged NONFINITE).
+ * flags[B] (device, NULL ok): |= NONFINITE; NEAR_TIE when the top-p boundary decision lies within
+ *    3e-7 Z of top_p Z (the masses are float32 exponentials summed exactly in 2^-40 fixed point,
+ *    so the decision can differ from exact arithmetic only there).
+ * One CTA per row: radix selection on the order-preserving integer key of the values (2 passes
+ *    per selection for bf16, 4 for f32) plus a maximum and a write pass -- every pass after the
+ *    first reads the row from L2.  Asynchronous on `stream`; no workspace.
+ * ------------------------------------------------------------------------- */
+msd_status msd_logits_process(const msd_logits* in, const msd_logits* out, int32_t B, int32_t rows, int64_t V,
+                              const msd_processors* proc, float* tau, uint32_t* flags, void* stream);
 
 /* ---------------------------------------------------------------------------
  * msd_lmhead_lse -- the step before the path, fused (Eq. 1

@@ -87,6 +87,8 @@ def lib() -> ctypes.CDLL:
     L.msd_pool_divergence.argtypes = [P, i32, i32, i32, i64, P, P, P, P, P]
     L.msd_draft_sample.restype = i32
     L.msd_draft_sample.argtypes = [P, i32, i32, i64, P, i32, P, P, P, P, P]
+    L.msd_logits_process.restype = i32
+    L.msd_logits_process.argtypes = [P, P, i32, i32, i64, P, P, P, P]
     L.msd_predict_chain_latency.restype = i32
     L.msd_predict_chain_latency.argtypes = [i32, P, P, i32, i32, i32, P]
     L.msd_select_chain.restype = i32
@@ -316,6 +318,32 @@ def draft_sample(drafter: torch.Tensor, u: Optional[torch.Tensor], row: int = 0,
                                 _ptr(out["flags"]), _stream(stream))
     _check(st, "msd_draft_sample")
     return out
+
+
+def logits_process(logits: torch.Tensor, rows: Optional[int] = None, V: Optional[int] = None, *,
+                   top_k: int = 0, top_p: float = 1.0, temperature: float = 1.0,
+                   out: Optional[torch.Tensor] = None, tau: Optional[torch.Tensor] = None,
+                   flags: Optional[torch.Tensor] = None, stream=None):
+    """msd_logits_process: top-k / top-p over rows [0, rows) of logits [B][R][ld] (P:150,
+    DESIGN.md R19 / R23).  Writes the processed rows (removed entries -inf) to `out` (a new
+    tensor shaped like `logits` when None; `out=logits` processes in place).  Returns
+    (out, tau [B][rows] f32, flags [B] int32)."""
+    B, R = logits.shape[0], logits.shape[1]
+    rows = R if rows is None else rows
+    V = logits.shape[2] if V is None else V
+    dev = logits.device
+    if out is None:
+        out = torch.empty_like(logits)
+    if tau is None:
+        tau = torch.empty((B, rows), dtype=torch.float32, device=dev)
+    if flags is None:
+        flags = torch.zeros((B,), dtype=torch.int32, device=dev)
+    di, do = logits_desc(logits), logits_desc(out)
+    pr = msd_processors(float(temperature), int(top_k), float(top_p))
+    st = lib().msd_logits_process(ctypes.byref(di), ctypes.byref(do), B, int(rows), int(V), ctypes.byref(pr),
+                                  _ptr(tau), _ptr(flags), _stream(stream))
+    _check(st, "msd_logits_process")
+    return out, tau, flags
 
 
 # ------------------------------------------------------------------ scheduler feed (host C)

@@ -287,7 +287,7 @@ msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B,
         if (!(proc->temperature > 0.f) || !(proc->temperature <= 1e6f) || !(1.f / proc->temperature <= 1e6f))
             return fail(MSD_E_ARG, "temperature %g outside (1e-6, 1e6]", (double)proc->temperature);
         if (proc->top_k != 0 || !(proc->top_p >= 1.f || proc->top_p <= 0.f))
-            return fail(MSD_E_ARG, "top_k / top_p are not supported (pass 0 / 1)");
+            return fail(MSD_E_ARG, "top_k / top_p: run msd_logits_process on every level first, then pass 0 / 1 here");
         inv_temp = 1.f / proc->temperature;
     }
     if (!levels) return fail(MSD_E_ARG, "levels is NULL");
@@ -460,6 +460,37 @@ msd_status msd_draft_sample(const msd_logits* drafter, int32_t row, int32_t B, i
     dp.u = u; dp.token = token; dp.lse = lse; dp.q_tok = q_tok; dp.flags = flags;
     cudaError_t e = launch_draft(dp, bf16, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "msd_draft launch");
+    return MSD_OK;
+}
+
+msd_status msd_logits_process(const msd_logits* in, const msd_logits* out, int32_t B, int32_t rows, int64_t V,
+                              const msd_processors* proc, float* tau, uint32_t* flags, void* stream) {
+    if (!in || !out || !proc) return fail(MSD_E_ARG, "in, out and proc are required");
+    if (B < 0 || rows < 1) return fail(MSD_E_ARG, "bad B=%d / rows=%d", B, rows);
+    if (V < 1 || V > ((int64_t)1 << 31) - 1) return fail(MSD_E_ARG, "V=%lld outside [1, 2^31)", (long long)V);
+    if (!(proc->temperature > 0.f) || !(proc->temperature <= 1e6f) || !(1.f / proc->temperature <= 1e6f))
+        return fail(MSD_E_ARG, "temperature %g outside (1e-6, 1e6]", (double)proc->temperature);
+    if (proc->top_k < 0) return fail(MSD_E_ARG, "top_k=%d < 0", proc->top_k);
+    if (B == 0) return MSD_OK;
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    int32_t bf16 = 0, bf16o = 0;
+    st = validate_levels(in, 1, rows, V, 0, 0, &bf16);
+    if (st != MSD_OK) return st;
+    st = validate_levels(out, 1, rows, V, 0, 0, &bf16o);
+    if (st != MSD_OK) return st;
+    if (bf16 != bf16o) return fail(MSD_E_DTYPE, "in and out dtypes differ");
+    ProcParams pp;
+    memset(&pp, 0, sizeof(pp));
+    pp.in = in->ptr; pp.out = const_cast<void*>(out->ptr);
+    pp.in_ld = in->ld; pp.in_bs = in->batch_stride; pp.out_ld = out->ld; pp.out_bs = out->batch_stride;
+    pp.B = B; pp.rows = rows; pp.V = V;
+    pp.inv_temp = 1.f / proc->temperature;
+    pp.top_k = proc->top_k;
+    pp.top_p = proc->top_p;
+    pp.tau = tau; pp.flags = flags;
+    cudaError_t e = launch_proc(pp, bf16, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "msd_proc launch");
     return MSD_OK;
 }
 

@@ -103,6 +103,19 @@ struct DraftParams {         // draft-side sampling step (msd_draft.cu)
     uint32_t* flags;
 };
 
+struct ProcParams {           // top-k / top-p logits processors (msd_proc.cu)
+    const void* in;
+    void* out;                // may equal in (in place)
+    int64_t in_ld, in_bs, out_ld, out_bs;
+    int32_t B, rows;
+    int64_t V;
+    float inv_temp;           // 1 / T (top-p masses are those of softmax(z / T))
+    int32_t top_k;            // 0 = off
+    float top_p;              // outside (0, 1) = off
+    float* tau;               // [B][rows] or NULL
+    uint32_t* flags;          // [B] or NULL
+};
+
 struct RollbackParams {
     msd_paged_kv kv[8];
     int32_t n_models, B;
@@ -135,6 +148,7 @@ cudaError_t launch_tail(const TailParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_rollback(const RollbackParams& p, cudaStream_t s);
 cudaError_t launch_pool(const PoolParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_draft(const DraftParams& p, int bf16, cudaStream_t s);
+cudaError_t launch_proc(const ProcParams& p, int bf16, cudaStream_t s);
 cudaError_t launch_lmhead(const LmHeadParams& p, cudaStream_t s);
 size_t lmhead_workspace(int32_t M, int64_t V, int nsm);
 
