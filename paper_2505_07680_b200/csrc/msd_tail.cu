@@ -158,7 +158,7 @@ __device__ __forceinline__ void load_vec(const Tin* row, int64_t e, int64_t Vend
 // takes the generic path) when the maximum is not finite.  Argmax only when `want_am`.
 __device__ bool slice_partial_bf16(const __nv_bfloat16* row, int64_t s0, int64_t s1, bool want_am, Partial* out) {
     const int lane = threadIdx.x & 31;
-    constexpr int VEC = 8, U = 4;   // vectors in flight per lane
+    constexpr int VEC = 8, U = 8;   // vectors in flight per lane
     uint32_t mx = 0xFF80FF80u;   // -inf pair
     for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
         uint4 v[U];
@@ -337,7 +337,7 @@ __device__ void pair_resid(const Tin* ra, const Tin* rb, const RowStat& A, const
     for (int s = warp; s < C; s += NWARP) {
         const int64_t s0 = (int64_t)s * vse, s1 = min(V, s0 + vse);
         double acc = 0.0;
-        constexpr int U = 2;    // vector pairs in flight per lane
+        constexpr int U = 4;    // vector pairs in flight per lane
         for (int64_t e0 = s0 + (int64_t)lane * VEC; e0 < s1; e0 += U * 32 * VEC) {
             float xa[U][VEC], xb[U][VEC];
 #pragma unroll
