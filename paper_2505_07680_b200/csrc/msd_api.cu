@@ -222,11 +222,16 @@ msd_status run_engine(const Engine& E) {
     }
 
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    // under stream capture (a CUDA graph) the events become external event-record nodes, which
+    // record on every replay (a plain record would only add a capture dependency)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(E.stream, &cap);
+    const unsigned rec_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
     {
         std::lock_guard<std::mutex> g(g_prof.mu);
         if (g_prof.on) {
             ev = prof_pair();
-            cudaEventRecord(ev.first, E.stream);
+            cudaEventRecordWithFlags(ev.first, E.stream, rec_flags);
         }
         g_prof.total_launches += 2;
     }
@@ -234,7 +239,7 @@ msd_status run_engine(const Engine& E) {
     if (e != cudaSuccess) return cuda_fail(e, "msd_core launch");
     if (ev.first) {
         std::lock_guard<std::mutex> g(g_prof.mu);
-        cudaEventRecord(ev.second, E.stream);
+        cudaEventRecordWithFlags(ev.second, E.stream, rec_flags);
         g_prof.pending.push_back(ev);
     }
     e = launch_tail(tp, E.bf16, E.stream);
