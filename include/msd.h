@@ -350,7 +350,7 @@ msd_status msd_debug_set_trace(void* dev_buf, size_t bytes);
  * isolation mode (0 = normal; 1 = pass 1 + ring only, results invalid; 4|1 = ring only; bits
  * 8..11 = L2 prefetch distance in items + 1, 0 = the default 2);
  * exact_draws: 1 = every residual / bonus draw takes the float64 exact path; z_safe: residual
- * mass below which a draw takes the exact path (default 0.05, R4; < 0 = default).
+ * mass below which a draw takes the exact path (default 0.01, R4; < 0 = default).
  * The outputs are identical for every pattern / stage choice and for exact_draws 0 / 1 outside
  * the documented near-tie bands.  Not thread-safe against concurrent calls. */
 msd_status msd_debug_set_knobs(int32_t pat_t, int32_t pat_r, int32_t stages, int32_t core_dbg,

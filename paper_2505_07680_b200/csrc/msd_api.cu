@@ -541,7 +541,7 @@ msd_status msd_debug_set_knobs(int32_t pat_t, int32_t pat_r, int32_t stages, int
     g_knobs.stages = stages;
     g_knobs.core_dbg = core_dbg;
     g_knobs.exact_draws = exact_draws ? 1 : 0;
-    g_knobs.z_safe = z_safe >= 0 ? z_safe : 0.05;
+    g_knobs.z_safe = z_safe >= 0 ? z_safe : 0.01;
     return MSD_OK;
 }
 

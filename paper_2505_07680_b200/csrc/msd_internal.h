@@ -138,7 +138,7 @@ struct LmHeadParams {        // fused lm_head GEMM + row normaliser (msd_lmhead.
 // Test / diagnostic overrides (msd_debug_set_knobs); the defaults are the release behaviour.
 struct DebugKnobs {
     int32_t pat_t = -1, pat_r = -1, stages = -1, core_dbg = 0, exact_draws = 0;
-    double z_safe = 0.05;
+    double z_safe = 0.01;
 };
 extern DebugKnobs g_knobs;
 

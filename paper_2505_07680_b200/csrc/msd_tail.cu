@@ -10,7 +10,7 @@
 // mass R_s of each 4096-entry vocabulary slice (and the slice partials from which
 // the bonus mass P_s follows).  A draw picks the slice from these (float64
 // prefix) and rescans only that slice in float64 (`draw_fast`).  When the
-// residual mass is small (Z < z_safe, default 0.05) or the target is within the margin of a
+// residual mass is small (Z < z_safe, default 0.01) or the target is within the margin of a
 // slice / token boundary, the fp32-derived slice masses are not
 // accurate enough relative to Z, so the whole row pair is recomputed in float64
 // (`draw_exact`, flagged MSD_F_EXACT_DRAW).  Rows at positions >= K (bonus rows,
@@ -38,9 +38,10 @@ constexpr double TIE_EPS = 1e-6;
 // (R4), far inside the margin.  Otherwise the exact path decides.
 constexpr double DRAW_MARGIN_REL = 2e-5, DRAW_MARGIN_ABS = 0.0;
 // u Z this close (relative to Z) to a slice boundary of the fp32-derived slice prefix: the slice
-// itself may be the wrong one (prefix error ~1e-7 Z), so the exact path re-selects it from
-// float64 slice masses
-constexpr double SLICE_MARGIN_REL = 1e-6;
+// itself may be the wrong one, so the exact path re-selects it from float64 slice masses.  The
+// prefix error relative to Z grows as the residual mass shrinks (~3e-8 / Z measured), so the
+// margin is max(1e-6, 1.5e-7 / Z): 5x the drift down to z_safe = 0.01
+constexpr double SLICE_MARGIN_REL = 1e-6, SLICE_MARGIN_Z = 1.5e-7;
 
 struct TailShared {
     RowStat row[MAXC][MAXL];      // row statistics of draft positions i < K (from the core partials)
@@ -664,7 +665,8 @@ __device__ int32_t draw_slices(bool resid, const Tin* ra, const Tin* rb, double 
     const int sel = sh.sel_slice;
     const double before = sh.sel_before, after = sh.sel_after;
     __syncthreads();
-    if (!exact && sel >= 0 && (u * Z - before < SLICE_MARGIN_REL * Z || after - u * Z < SLICE_MARGIN_REL * Z))
+    const double smarg = fmax(SLICE_MARGIN_REL * Z, SLICE_MARGIN_Z);
+    if (!exact && sel >= 0 && (u * Z - before < smarg || after - u * Z < smarg))
         return -1;      // next to a slice boundary: the caller takes the exact path
     if (sel < 0) {  // u*Z beyond the total (rounding): clamp to the last positive entry
         *tie = true;
