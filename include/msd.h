@@ -187,6 +187,25 @@ msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B,
                                  const msd_processors* proc, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * msd_chain_verify_lse -- msd_chain_verify when the producer of the logits already knows every
+ * draft-position row's normaliser (the lm_head epilogue reduces each row to
+ * LSE_r = log sum_v exp z_rv on the fly, Eq. 1).  lse (device float64, [L][B][K]): the
+ * natural-log normaliser of rows i < K of every level, of the logits exactly as supplied (T = 1).
+ * The core kernel then needs no cross-CTA exchange of slice records: pass 2 (DTV, residual masses)
+ * starts as soon as this CTA's pass 1 is done.  Outputs, workspace and every other argument as
+ * msd_chain_verify; acceptance, KL and the draws still use the kernels' own float64 normalisers,
+ * so a wrong lse changes only DTV and the residual slice masses (caller contract: lse must be the
+ * normaliser of the supplied rows to float64 precision).
+ * ------------------------------------------------------------------------- */
+msd_status msd_chain_verify_lse(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                                const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                                int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                                int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                                int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                                msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                                const double* lse, void* stream);
+
+/* ---------------------------------------------------------------------------
  * msd_kv_rollback -- batched rollback of each model's paged KV state
  * (§4.4: logical rollback of the last r_b entries, Eq. 8; physical
  * reclamation, Eq. 9, generalised to per-sequence release of whole blocks).

@@ -74,6 +74,9 @@ def lib() -> ctypes.CDLL:
     L.msd_chain_verify_proc.restype = i32
     L.msd_chain_verify_proc.argtypes = [P, i32, i32, i32, i64, P, P, P, i32, i32, i32,
                                         P, P, P, P, P, P, P, P, P, P, sz, P, P]
+    L.msd_chain_verify_lse.restype = i32
+    L.msd_chain_verify_lse.argtypes = [P, i32, i32, i32, i64, P, P, P, i32, i32, i32,
+                                       P, P, P, P, P, P, P, P, P, P, sz, P, P]
     L.msd_verify_level.restype = i32
     L.msd_verify_level.argtypes = [msd_logits, msd_logits, i32, i32, i64, P, P, P, P, i32, i32,
                                    P, P, P, P, P, P, P, P, sz, P]
@@ -162,7 +165,8 @@ class ChainVerify:
     def __init__(self, levels: Sequence[torch.Tensor], draft: torch.Tensor, u_acc=None, u_emit=None,
                  *, V: Optional[int] = None, greedy=False, intermediate_bonus=True,
                  draft_fed: Optional[int] = None, pos_outputs=True, rollback=True, stats=True,
-                 ws: Optional[torch.Tensor] = None, temperature: Optional[float] = None):
+                 ws: Optional[torch.Tensor] = None, temperature: Optional[float] = None,
+                 lse: Optional[torch.Tensor] = None):
         dev = draft.device
         _check(lib().msd_init(), "msd_init")   # one-time device setup, outside any graph capture
         self.L = len(levels)
@@ -193,7 +197,15 @@ class ChainVerify:
                       _ptr(self.commit_tok), _ptr(self.commit_len), _ptr(self.rollback),
                       _ptr(self.pos_dtv), _ptr(self.pos_kl), _ptr(self.stats), _ptr(self.flags),
                       _ptr(self.ws), self.ws.numel()]
-        if temperature is None:
+        if lse is not None:     # producer-supplied row normalisers (msd_chain_verify_lse), [L][B][K] f64
+            if temperature is not None:
+                raise MsdError("lse and temperature cannot be combined")
+            if lse.dtype != torch.float64 or tuple(lse.shape) != (L, B, K) or not lse.is_contiguous():
+                raise MsdError("lse must be a contiguous float64 [L][B][K] tensor")
+            self.lse = lse
+            self._args.append(_ptr(lse))
+            self._fn = lib().msd_chain_verify_lse
+        elif temperature is None:
             self._fn = lib().msd_chain_verify
         else:     # logits processor (msd_chain_verify_proc): softmax(z / T) at every level
             self._proc = msd_processors(float(temperature), 0, 1.0)

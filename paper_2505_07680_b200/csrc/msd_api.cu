@@ -138,6 +138,7 @@ struct Engine {
     size_t ws_bytes;
     cudaStream_t stream;
     float inv_temp;     // logits processor: 1 / temperature (1 = none)
+    const double* lse;  // producer-supplied row normalisers [L][B][K] (msd_chain_verify_lse) or NULL
 };
 
 msd_status validate_levels(const msd_logits* lv, int32_t L, int32_t K, int64_t V, int32_t ibonus,
@@ -196,6 +197,7 @@ msd_status run_engine(const Engine& E) {
     cp.trace = (g_trace && g_trace_items >= (size_t)cp.n_items) ? g_trace : nullptr;
     cp.dbg = g_knobs.core_dbg;
     cp.inv_temp = E.inv_temp;
+    cp.lse = E.lse;
 
     TailParams tp;
     memset(&tp, 0, sizeof(tp));
@@ -280,13 +282,13 @@ msd_status msd_chain_verify(const msd_logits* levels, int32_t L, int32_t B, int3
                                  pos_kl, stats, flags, ws, ws_bytes, nullptr, stream);
 }
 
-msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
-                                 const int32_t* draft_tok, const float* u_acc, const float* u_emit,
-                                 int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
-                                 int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
-                                 int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
-                                 msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
-                                 const msd_processors* proc, void* stream) {
+static msd_status chain_verify_impl(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                                    const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                                    int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                                    int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                                    int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                                    msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                                    const msd_processors* proc, const double* lse, void* stream) {
     float inv_temp = 1.f;
     if (proc) {
         if (!(proc->temperature > 0.f) || !(proc->temperature <= 1e6f) || !(1.f / proc->temperature <= 1e6f))
@@ -334,7 +336,33 @@ msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B,
     E.ws = ws; E.ws_bytes = ws_bytes;
     E.stream = reinterpret_cast<cudaStream_t>(stream);
     E.inv_temp = inv_temp;
+    E.lse = lse;
     return run_engine(E);
+}
+
+msd_status msd_chain_verify_proc(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                                 const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                                 int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                                 int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                                 int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                                 msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                                 const msd_processors* proc, void* stream) {
+    return chain_verify_impl(levels, L, B, K, V, draft_tok, u_acc, u_emit, mode, intermediate_bonus, draft_fed,
+                             n_acc, m_cand, commit_tok, commit_len, rollback, pos_dtv, pos_kl, stats, flags, ws,
+                             ws_bytes, proc, nullptr, stream);
+}
+
+msd_status msd_chain_verify_lse(const msd_logits* levels, int32_t L, int32_t B, int32_t K, int64_t V,
+                                const int32_t* draft_tok, const float* u_acc, const float* u_emit,
+                                int32_t mode, int32_t intermediate_bonus, int32_t draft_fed,
+                                int32_t* n_acc, int32_t* m_cand, int32_t* commit_tok,
+                                int32_t* commit_len, int32_t* rollback, float* pos_dtv, float* pos_kl,
+                                msd_pair_stats* stats, uint32_t* flags, void* ws, size_t ws_bytes,
+                                const double* lse, void* stream) {
+    if (!lse) return fail(MSD_E_ARG, "lse is NULL");
+    return chain_verify_impl(levels, L, B, K, V, draft_tok, u_acc, u_emit, mode, intermediate_bonus, draft_fed,
+                             n_acc, m_cand, commit_tok, commit_len, rollback, pos_dtv, pos_kl, stats, flags, ws,
+                             ws_bytes, nullptr, lse, stream);
 }
 
 msd_status msd_verify_level(msd_logits q, msd_logits p, int32_t B, int32_t K, int64_t V,

@@ -391,7 +391,9 @@ struct Cursor {
     }
 };
 
-template <typename Tin, int L, bool GREEDY>
+// LSE: producer-supplied row normalisers (msd_chain_verify_lse), a separate instantiation so the
+// exchange path's register allocation is untouched
+template <typename Tin, int L, bool GREEDY, bool LSE>
 __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
     constexpr int VEC = Elem<Tin>::VEC;
     constexpr int NV = CET / VEC;           // 2 (bf16) or 4 (f32) vectors per thread and row
@@ -1058,6 +1060,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             item(j, u, b, i);
             const int k = j & (NQ - 1);
             if (lane == 0) stamp(j, 6);
+            // producer-supplied normalisers: lane l's row, in flight while the pass-1 warps finish
+            double lz = 0.0;
+            if (LSE && lane < L) lz = __ldg(p.lse + ((size_t)lane * p.B + b) * p.K + i);
             // the other slices of the unit are published around the time this one is: poll only
             // from then on (polls steal issue slots and L2 bandwidth)
             mbar_wait_lat(&c.pub[k], (uint32_t)((j / NQ) & 1));
@@ -1065,7 +1070,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             PROF(4)
             // stage the unit's records; a record whose sum is still 0 is not yet visible
             const unsigned long long* pm = reinterpret_cast<const unsigned long long*>(p.partms) + (size_t)u * LC;
-            while (true) {
+            // producer-supplied row normalisers (msd_chain_verify_lse): nothing to exchange
+            while (!LSE) {
                 // all loads in flight before any use (one round trip), then stage in smem
                 constexpr int MAXB = FBUF / 32;
                 unsigned long long rr[MAXB];
@@ -1098,6 +1104,23 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             // reference R_l (fp32).  A slice reference more than 2^127 above R_l, or a masked
             // own slice, falls back to the maximum reference.
             float Rl[L], Sl[L];
+            if (LSE) {
+                // reference: this CTA's own maximum of the row (its pass-1 warps' maxima); the
+                // normaliser relative to it, exp(lse - ref sc) >= 1, from the supplied float64 LSE
+                // (lane l computes row l, then every lane gets all rows)
+                float mr = -INFINITY;
+                if (lane < L)
+                    for (int w = 0; w < NW1; ++w)
+                        if ((amask >> (w % NCW)) & 1u) mr = fmaxf(mr, c.wmx[k][lane][w]);
+                if (!(mr > NEG_MASKED)) mr = (float)(lz / (double)sc);
+                const double x = (double)mr * (double)sc - lz;       // <= 0 up to the rounding of mr
+                const float sn = lane < L ? (x <= 0.0 ? (float)(1.0 / dexp_neg(x)) : (float)dexp_neg(-x)) : 0.f;
+#pragma unroll
+                for (int l = 0; l < L; ++l) {
+                    Rl[l] = __shfl_sync(0xffffffffu, mr, l);
+                    Sl[l] = __shfl_sync(0xffffffffu, sn, l);
+                }
+            } else {
 #pragma unroll
             for (int l = 0; l < L; ++l) {
                 Rl[l] = __uint_as_float((uint32_t)fb[l * C + NH * s]);   // first tail slice's record
@@ -1144,6 +1167,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
                 for (int l = 0; l < L; ++l) Sl[l] = warp_sum(Sl[l]);
             }
+            }   // exchange records
             PROF(1)
             if (j >= NQ) mbar_wait(&c.rowf_empty[k], (uint32_t)(((j / NQ) - 1) & 1));
             PROF(2)
@@ -1220,7 +1244,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 }
 
 
-template <typename Tin, int L, bool G>
+template <typename Tin, int L, bool G, bool LSE>
 static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     CoreParams p = p0;
     const int ES = (int)sizeof(Tin);
@@ -1243,7 +1267,7 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
     // L2 prefetch distance: 2 items (core_dbg bits 8..11 = distance + 1 override it)
     p.pf_dist = ((g_knobs.core_dbg >> 8) & 15) ? ((g_knobs.core_dbg >> 8) & 15) - 1 : 2;
     const size_t smem = ctl + (size_t)S * stage_bytes + 128;
-    auto k = core_kernel<Tin, L, G>;
+    auto k = core_kernel<Tin, L, G, LSE>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0, occ = 0;
@@ -1266,7 +1290,10 @@ static cudaError_t launch_one(const CoreParams& p0, cudaStream_t s) {
 
 cudaError_t launch_core(const CoreParams& p, int bf16, int greedy, cudaStream_t s) {
 #define MSD_CASE(TY, LL)                                                         \
-    if (p.L == LL) return greedy ? launch_one<TY, LL, true>(p, s) : launch_one<TY, LL, false>(p, s);
+    if (p.L == LL) {                                                             \
+        if (p.lse) return greedy ? launch_one<TY, LL, true, true>(p, s) : launch_one<TY, LL, false, true>(p, s); \
+        return greedy ? launch_one<TY, LL, true, false>(p, s) : launch_one<TY, LL, false, false>(p, s);         \
+    }
     if (bf16) {
         MSD_CASE(__nv_bfloat16, 2)
         MSD_CASE(__nv_bfloat16, 3)

@@ -43,6 +43,7 @@ struct CoreParams {
     unsigned long long* trace;   // debug: 16 globaltimer stamps per item, or NULL
     int32_t dbg;                 // debug isolation mode (msd_debug_set_knobs): 0 = normal
     float inv_temp;              // 1 / temperature of the logits processor (1 = none)
+    const double* lse;           // [L][B][K] producer-supplied row normalisers, or NULL (exchange)
 };
 
 // exp of every bf16 value in float64 (65536 entries), filled once per device by msd_init (or

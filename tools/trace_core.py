@@ -4,10 +4,13 @@ os.environ.setdefault("MSD_LIB", "libmsd_trace.so")   # stamps are compiled in w
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2505_07680_b200 import api, synth
-name = sys.argv[1] if len(sys.argv) > 1 else "llama3"
+name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "llama3"
 c = synth.CONFIGS[name]
 inp = synth.gauss_chain(c["B"], c["V"], c["K"], c["L"], c["sigmas"], s=c["s"], seed=c["seed"], device="cuda", dtype=c["dtype"])
-cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"])
+kw = {}
+if "--lse" in sys.argv:   # producer-supplied normalisers (msd_chain_verify_lse): no exchange
+    kw["lse"] = torch.stack([torch.logsumexp(t[:, :c["K"], :c["V"]].float(), dim=-1).double() for t in inp.levels]).contiguous()
+cv = api.ChainVerify(inp.levels, inp.draft, inp.u_acc, inp.u_emit, V=c["V"], **kw)
 def geo(V, VS=4096, REF=148):
     """core slices per unit: ceil(C / 2) CTAs for the tail's C slices (msd_common.cuh)"""
     used = lambda cc: (REF // ((cc + 1) // 2)) * ((cc + 1) // 2)
