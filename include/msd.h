@@ -342,6 +342,14 @@ msd_status msd_logits_process(const msd_logits* in, const msd_logits* out, int32
  * bytes (per-row partial records).  Asynchronous on `stream`.
  * ------------------------------------------------------------------------- */
 size_t msd_lmhead_workspace(int32_t M, int64_t V);
+/* msd_lmhead_logits -- the same GEMM when the verify needs the full distributions (DTV, residual
+ * draws): the epilogue also writes the logits, rounded to bf16, to logits [M][ldz] (16-byte
+ * aligned rows, ldz >= V), and reduces the *written* values, so lse64 [M] (device float64) is the
+ * normaliser of exactly the tensor msd_chain_verify_lse then reads (its `lse` input) -- the verify
+ * core needs no exchange.  z_cand as msd_lmhead_lse (of the rounded logits); ws as msd_lmhead_lse. */
+msd_status msd_lmhead_logits(const void* H, const void* W, int32_t M, int32_t D, int64_t V, const int32_t* cand,
+                             void* logits, int64_t ldz, double* lse64, float* z_cand, void* ws, size_t ws_bytes,
+                             void* stream);
 msd_status msd_lmhead_lse(const void* H, const void* W, int32_t M, int32_t D, int64_t V, const int32_t* cand,
                           float* lse, float* z_cand, void* ws, size_t ws_bytes, void* stream);
 

@@ -105,6 +105,8 @@ def lib() -> ctypes.CDLL:
     L.msd_init.argtypes = []
     L.msd_lmhead_workspace.restype = sz
     L.msd_lmhead_workspace.argtypes = [i32, i64]
+    L.msd_lmhead_logits.restype = i32
+    L.msd_lmhead_logits.argtypes = [P, P, i32, i32, i64, P, P, i64, P, P, P, sz, P]
     L.msd_lmhead_lse.restype = i32
     L.msd_lmhead_lse.argtypes = [P, P, i32, i32, i64, P, P, P, P, sz, P]
     L.msd_prof_enable.restype = i32
@@ -410,6 +412,27 @@ def lmhead_lse(H: torch.Tensor, W: torch.Tensor, cand: Optional[torch.Tensor] = 
     _check(lib().msd_lmhead_lse(H.data_ptr(), W.data_ptr(), M, D, V, _ptr(cand), lse.data_ptr(), zc.data_ptr(),
                                 ws.data_ptr(), ws.numel(), _stream(stream)), "msd_lmhead_lse")
     return dict(lse=lse, z_cand=zc, ws=ws)
+
+
+def lmhead_logits(H: torch.Tensor, W: torch.Tensor, cand: Optional[torch.Tensor] = None,
+                  out: Optional[torch.Tensor] = None, lse64: Optional[torch.Tensor] = None, stream=None) -> dict:
+    """msd_lmhead_logits: logits = H W^T written in bf16 (out: [M, ldz] view, new [M, V8] when None)
+    plus the float64 normaliser of the written rows (the `lse` msd_chain_verify_lse consumes)."""
+    if H.dtype != torch.bfloat16 or W.dtype != torch.bfloat16 or not H.is_contiguous() or not W.is_contiguous():
+        raise MsdError("H and W must be contiguous bf16")
+    M, D = H.shape
+    V = W.shape[0]
+    dev = H.device
+    if out is None:
+        out = torch.empty((M, (V + 7) // 8 * 8), dtype=torch.bfloat16, device=dev)
+    if lse64 is None:
+        lse64 = torch.empty(M, dtype=torch.float64, device=dev)
+    zc = torch.empty(M, dtype=torch.float32, device=dev)
+    ws = torch.empty(max(1, int(lib().msd_lmhead_workspace(M, V))), dtype=torch.uint8, device=dev)
+    _check(lib().msd_lmhead_logits(H.data_ptr(), W.data_ptr(), M, D, V, _ptr(cand), out.data_ptr(), out.stride(0),
+                                   lse64.data_ptr(), zc.data_ptr(), ws.data_ptr(), ws.numel(), _stream(stream)),
+           "msd_lmhead_logits")
+    return dict(logits=out, lse64=lse64, z_cand=zc, ws=ws)
 
 
 def prof_enable(on=True):

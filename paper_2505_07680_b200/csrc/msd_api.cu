@@ -545,8 +545,35 @@ msd_status msd_lmhead_lse(const void* H, const void* W, int32_t M, int32_t D, in
     if (st != MSD_OK) return st;
     if (ws_bytes < msd_lmhead_workspace(M, V)) return fail(MSD_E_WORKSPACE, "workspace too small");
     LmHeadParams p;
+    memset(&p, 0, sizeof(p));
     p.H = H; p.W = W; p.M = M; p.D = D; p.V = V; p.cand = cand; p.lse = lse; p.z_cand = z_cand;
     p.ws = ws; p.ws_bytes = ws_bytes;
+    {
+        std::lock_guard<std::mutex> g(g_prof.mu);
+        g_prof.total_launches += 2;
+    }
+    cudaError_t e = launch_lmhead(p, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "msd_lmhead launch");
+    return MSD_OK;
+}
+
+msd_status msd_lmhead_logits(const void* H, const void* W, int32_t M, int32_t D, int64_t V, const int32_t* cand,
+                             void* logits, int64_t ldz, double* lse64, float* z_cand, void* ws, size_t ws_bytes,
+                             void* stream) {
+    if (M < 0 || D < 64 || D % 64 || V < 1 || V > ((int64_t)1 << 31) - 1 || ldz < V)
+        return fail(MSD_E_ARG, "bad M=%d / D=%d (multiple of 64) / V=%lld / ldz", M, D, (long long)V);
+    if (M == 0) return MSD_OK;
+    if (!H || !W || !logits || !lse64 || !ws) return fail(MSD_E_ARG, "H, W, logits, lse64 and ws are required");
+    if (((uintptr_t)H) % 16 || ((uintptr_t)W) % 16 || ((uintptr_t)logits) % 16 || (ldz * 2) % 16)
+        return fail(MSD_E_ALIGN, "H, W and the logit rows must be 16-byte aligned");
+    msd_status st = check_arch();
+    if (st != MSD_OK) return st;
+    if (ws_bytes < msd_lmhead_workspace(M, V)) return fail(MSD_E_WORKSPACE, "workspace too small");
+    LmHeadParams p;
+    memset(&p, 0, sizeof(p));
+    p.H = H; p.W = W; p.M = M; p.D = D; p.V = V; p.cand = cand; p.lse = nullptr; p.z_cand = z_cand;
+    p.ws = ws; p.ws_bytes = ws_bytes;
+    p.logits = logits; p.ldz = ldz; p.lse64 = lse64;
     {
         std::lock_guard<std::mutex> g(g_prof.mu);
         g_prof.total_launches += 2;

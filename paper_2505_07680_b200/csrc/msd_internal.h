@@ -130,10 +130,13 @@ struct LmHeadParams {        // fused lm_head GEMM + row normaliser (msd_lmhead.
     int32_t M, D;
     int64_t V;
     const int32_t* cand;     // [M] or NULL
-    float* lse;              // [M]
+    float* lse;              // [M] or NULL
     float* z_cand;           // [M] or NULL
     void* ws;
     size_t ws_bytes;
+    void* logits;            // [M][ldz] bf16 output (msd_lmhead_logits) or NULL (never written)
+    int64_t ldz;
+    double* lse64;           // [M] float64 LSE of the written (bf16-rounded) logits, or NULL
 };
 
 // Test / diagnostic overrides (msd_debug_set_knobs); the defaults are the release behaviour.

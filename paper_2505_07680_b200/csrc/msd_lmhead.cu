@@ -70,7 +70,8 @@ constexpr uint32_t LM_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(L
 
 __global__ void __launch_bounds__(LM_THREADS, 1)
 lmhead_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int32_t M,
-              int32_t D, int64_t V, int32_t parts, const int32_t* cand, LmPart* out) {
+              int32_t D, int64_t V, int32_t parts, const int32_t* cand, LmPart* out,
+              __nv_bfloat16* logits, int64_t ldz) {
     extern __shared__ __align__(1024) unsigned char lm_smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(lm_smem_raw) + 1023) & ~(uintptr_t)1023);
     unsigned char* sA = smem;
@@ -191,6 +192,29 @@ lmhead_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
                 const int64_t c0 = n0 + ch * 32;
                 // columns past the vocabulary (TMA zero fill of the last tile) do not count
                 const int nv = (int)max((int64_t)0, min((int64_t)32, V - c0));
+                if (logits) {
+                    // the logits are emitted in bf16 and everything below (maximum, normaliser,
+                    // candidate) is computed from the emitted values, so the LSE is that of the
+                    // tensor the verify reads
+                    uint32_t w[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(w[k]) : "f"(v[2 * k + 1]), "f"(v[2 * k]));
+                        v[2 * k] = __uint_as_float(w[k] << 16);
+                        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+                    }
+                    if (r < M) {
+                        __nv_bfloat16* dst = logits + (int64_t)r * ldz + c0;
+                        if (nv == 32) {
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4)
+                                reinterpret_cast<uint4*>(dst)[q4] = make_uint4(w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+                        } else {
+                            for (int k = 0; k < nv; ++k)
+                                dst[k] = __ushort_as_bfloat16((unsigned short)(k & 1 ? w[k / 2] >> 16 : w[k / 2] & 0xffffu));
+                        }
+                    }
+                }
                 float cm = -INFINITY;
 #pragma unroll
                 for (int k = 0; k < 32; ++k)
@@ -231,7 +255,7 @@ lmhead_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
 }
 
 // row normaliser and candidate logit from the parts (fixed order, float64)
-__global__ void lmhead_combine(const LmPart* in, int32_t M, int32_t parts, float* lse, float* zc) {
+__global__ void lmhead_combine(const LmPart* in, int32_t M, int32_t parts, float* lse, float* zc, double* lse64) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= M) return;
     float m = -INFINITY;
@@ -243,7 +267,9 @@ __global__ void lmhead_combine(const LmPart* in, int32_t M, int32_t parts, float
         if (q.m > -INFINITY) s += q.s * exp((double)q.m - (double)m);
         if (q.has_cand) z = q.zc;
     }
-    lse[r] = (float)((double)m + log(s));
+    const double l = (double)m + log(s);
+    if (lse) lse[r] = (float)l;
+    if (lse64) lse64[r] = l;
     if (zc) zc[r] = z;
 }
 
@@ -301,10 +327,11 @@ cudaError_t launch_lmhead(const LmHeadParams& p, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(lmhead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     LmPart* parts_buf = reinterpret_cast<LmPart*>(p.ws);
-    lmhead_kernel<<<mtiles * parts, LM_THREADS, smem, s>>>(ma, mb, p.M, p.D, p.V, parts, p.cand, parts_buf);
+    lmhead_kernel<<<mtiles * parts, LM_THREADS, smem, s>>>(ma, mb, p.M, p.D, p.V, parts, p.cand, parts_buf,
+                                                           reinterpret_cast<__nv_bfloat16*>(p.logits), p.ldz);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    lmhead_combine<<<(p.M + 255) / 256, 256, 0, s>>>(parts_buf, p.M, parts, p.lse, p.z_cand);
+    lmhead_combine<<<(p.M + 255) / 256, 256, 0, s>>>(parts_buf, p.M, parts, p.lse, p.z_cand, p.lse64);
     return cudaGetLastError();
 }
 

@@ -55,3 +55,40 @@ def test_lmhead_lse_llama3_shape_sampled_rows():
     # the Llama-3 verify batch: B = 512 requests x R = 8 rows, hidden 4096, vocabulary 128256
     H, W, cand = _case(4096, 4096, 128256, seed=3)
     _check(H, W, cand, [0, 1, 127, 128, 2049, 4095])
+
+
+# ---------------------------------------------------------------- the fused pipeline (NEXT-2)
+def test_lmhead_logits_feed_the_exchange_free_verify():
+    # per level l: hidden states H_l [B * rows_l, D] and its own vocabulary projection W_l; the
+    # lm_head kernel writes bf16 logits and the float64 LSE of exactly those logits, which
+    # msd_chain_verify_lse consumes (no cross-CTA exchange in the verify core).  The verify result
+    # must equal the oracle's on the same bf16 logits.
+    from paper_2505_07680_b200 import synth
+    from tests._parity import assert_parity, run_oracle
+    B, K, L, D, V = 6, 5, 3, 256, 32003
+    g = torch.Generator().manual_seed(7)
+    Hb = torch.randn((B, K + L - 1, D), generator=g)
+    W0 = torch.randn((V, D), generator=g) * (3.0 / D ** 0.5)
+    levels, lses = [], []
+    for l in range(L):
+        rows = K + l
+        # the levels share the target's projection up to a perturbation (a chain of related models)
+        W = (W0 + torch.randn((V, D), generator=g) * ((0.35 * (L - 1 - l)) / D ** 0.5)).to(torch.bfloat16).cuda()
+        H = Hb[:, :rows].reshape(B * rows, D).to(torch.bfloat16).cuda().contiguous()
+        out = api.lmhead_logits(H, W)
+        torch.cuda.synchronize()
+        z = out["logits"].view(B, rows, -1)
+        levels.append(z)
+        lses.append(out["lse64"].view(B, rows)[:, :K])
+        ref = torch.logsumexp(z[:, :, :V].double(), dim=-1)
+        assert float((out["lse64"].view(B, rows) - ref).abs().max()) < 2e-6      # LSE of the written logits
+    lse = torch.stack(lses).contiguous()
+    draft = synth.draft_tokens(levels[0], K, V, seed=3)
+    gu = torch.Generator().manual_seed(9)
+    ua = torch.rand((L - 1, B, K + L - 1), generator=gu).cuda()
+    ue = torch.rand((L - 1, B, K + L - 1), generator=gu).cuda()
+    inp = synth.ChainInputs(levels=levels, draft=draft, u_acc=ua, u_emit=ue, V=V, K=K)
+    cv = api.ChainVerify(levels, draft, ua, ue, V=V, lse=lse)
+    cv()
+    torch.cuda.synchronize()
+    assert_parity(cv.outputs(), run_oracle(inp))

@@ -37,11 +37,16 @@ def fused():
 def cublas():
     z = H @ W.t()
     torch.logsumexp(z.float(), dim=1)
+out_z = torch.empty((M, (V + 7) // 8 * 8), dtype=torch.bfloat16, device="cuda")
+def fused_logits():
+    ws["l"] = api.lmhead_logits(H, W, cand, out=out_z)
 t_f = timeit(fused)
+t_l = timeit(fused_logits)
 t_c = timeit(cublas)
 ref = torch.logsumexp((H @ W.t()).float(), dim=1)
 err = (ws["o"]["lse"] - ref).abs().max().item()
 print(json.dumps({"M": M, "D": D, "V": V, "fused_ms": t_f, "fused_tflops": flops / t_f / 1e9,
                   "frac_of_sustained_bf16": flops / t_f / 1e9 / peaks["bf16_tflops_sustained"],
+                  "fused_with_bf16_logits_written_ms": t_l, "fused_with_logits_tflops": flops / t_l / 1e9,
                   "cublas_matmul_plus_logsumexp_ms": t_c, "max_abs_lse_diff_vs_cublas": err,
                   "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}))
