@@ -82,6 +82,9 @@ lmhead_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
     uint64_t* tfull = bars + 2 * LM_STAGES;
     uint64_t* tempty = bars + 2 * LM_STAGES + 2;
     uint32_t* taddr_s = reinterpret_cast<uint32_t*>(bars + 2 * LM_STAGES + 4);
+    // per epilogue warp: a 32-row x 32-column bf16 chunk (rows padded to 17 words) staged so the
+    // logit stores go out as whole 64-byte row segments
+    uint32_t* zstage = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(bars) + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mt = blockIdx.x / parts, part = blockIdx.x % parts;
@@ -203,16 +206,26 @@ lmhead_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
                         v[2 * k] = __uint_as_float(w[k] << 16);
                         v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
                     }
-                    if (r < M) {
-                        __nv_bfloat16* dst = logits + (int64_t)r * ldz + c0;
-                        if (nv == 32) {
+                    if (nv == 32) {
+                        uint32_t* st = zstage + (warp - 2) * (32 * 17);
 #pragma unroll
-                            for (int q4 = 0; q4 < 4; ++q4)
-                                reinterpret_cast<uint4*>(dst)[q4] = make_uint4(w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
-                        } else {
-                            for (int k = 0; k < nv; ++k)
-                                dst[k] = __ushort_as_bfloat16((unsigned short)(k & 1 ? w[k / 2] >> 16 : w[k / 2] & 0xffffu));
+                        for (int k = 0; k < 16; ++k) st[lane * 17 + k] = w[k];
+                        __syncwarp();
+                        // 8 rows per store instruction: lane -> (row 8 q + lane / 4, 16-byte part lane % 4)
+#pragma unroll
+                        for (int qq = 0; qq < 4; ++qq) {
+                            const int rl = qq * 8 + (lane >> 2), part = lane & 3;
+                            const int rg = m0 + q * 32 + rl;
+                            const uint32_t* sr = st + rl * 17 + part * 4;
+                            if (rg < M)
+                                *reinterpret_cast<uint4*>(logits + (int64_t)rg * ldz + c0 + part * 8) =
+                                    make_uint4(sr[0], sr[1], sr[2], sr[3]);
                         }
+                        __syncwarp();
+                    } else if (r < M) {
+                        __nv_bfloat16* dst = logits + (int64_t)r * ldz + c0;
+                        for (int k = 0; k < nv; ++k)
+                            dst[k] = __ushort_as_bfloat16((unsigned short)(k & 1 ? w[k / 2] >> 16 : w[k / 2] & 0xffffu));
                     }
                 }
                 float cm = -INFINITY;
@@ -323,7 +336,7 @@ cudaError_t launch_lmhead(const LmHeadParams& p, cudaStream_t s) {
     if (!make_map(&ma, p.H, (uint64_t)p.D, (uint64_t)p.M, LM_BM) ||
         !make_map(&mb, p.W, (uint64_t)p.D, (uint64_t)p.V, LM_BN))
         return cudaErrorInvalidValue;
-    const size_t smem = 1024 + LM_STAGES * (LM_A_BYTES + LM_B_BYTES) + 256;
+    const size_t smem = 1024 + LM_STAGES * (LM_A_BYTES + LM_B_BYTES) + 256 + 4 * 32 * 17 * 4;
     cudaError_t e = cudaFuncSetAttribute(lmhead_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     LmPart* parts_buf = reinterpret_cast<LmPart*>(p.ws);
