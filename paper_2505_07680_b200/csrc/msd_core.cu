@@ -526,14 +526,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         const int k = j & (NQ - 1);
         const int r1 = j & (R1 - 1);
         // the NSPLIT pass-1 warps of region w (each with its own warp maximum)
-        float Sh[NSPLIT], Kh[NSPLIT], wmh[NSPLIT];
-        double Sdh[NSPLIT];
+        float Sh[NSPLIT], wmh[NSPLIT], cmh[NSPLIT];
+        double Sdh[NSPLIT], Khd[NSPLIT];
         int ah[NSPLIT];
         float wm = -INFINITY;
 #pragma unroll
         for (int h = 0; h < NSPLIT; ++h) {
-            Sh[h] = Kh[h] = 0.f;
-            Sdh[h] = 0.0;
+            Sh[h] = cmh[h] = 0.f;
+            Sdh[h] = Khd[h] = 0.0;
             wmh[h] = -INFINITY;
             ah[h] = 0x7fffffff;
             if (act) {
@@ -542,8 +542,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 const float4 k4 = *reinterpret_cast<const float4*>(&c.r1K[r1][l][wq][0]);
                 Sh[h] = (s4.x + s4.y) + (s4.z + s4.w);
                 Sdh[h] = ((double)s4.x + (double)s4.y) + ((double)s4.z + (double)s4.w);
-                Kh[h] = (k4.x + k4.y) + (k4.z + k4.w);
+                Khd[h] = ((double)k4.x + (double)k4.y) + ((double)k4.z + (double)k4.w);
                 wmh[h] = c.wmx[k][l][wq];
+                if (l > 0) cmh[h] = wmh[h] - c.wmx[k][l - 1][wq];   // the centring offset m_l - m_{l-1}
                 if (GREEDY) ah[h] = c.r1A[r1][l][wq];
                 wm = max_nan_f32(wm, wmh[h]);
             }
@@ -558,7 +559,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) msl = max_nan_f32(msl, __shfl_xor_sync(0xffffffffu, msl, o));
         // each warp's records scaled to the slice maximum (factor 1 when the warp holds it)
-        float Sx = 0.f, Kx = 0.f, fh[NSPLIT];
+        float Sx = 0.f, fh[NSPLIT];
+        double Kxd = 0.0;
         int ax = 0x7fffffff;
 #pragma unroll
         for (int h = 0; h < NSPLIT; ++h) {
@@ -566,8 +568,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             if (!(wmh[h] > NEG_MASKED)) f = (act && !(msl > NEG_MASKED)) ? 1.f : 0.f;   // masked warp region
             fh[h] = f;
             Sx += Sh[h] * f;
-            // KL numerator sum e (z_l - z_{l-1}) of the raw logit differences (no shift term)
-            if (l > 0 && f != 0.f) Kx += f * Kh[h];
+            // KL numerator sum e (z_l - z_{l-1}) in float64: centred sum plus offset times the sum
+            if (l > 0 && f != 0.f) Kxd += (double)f * (Khd[h] + (double)cmh[h] * Sdh[h]);
             if (wmh[h] == msl) ax = min(ax, ah[h]);
         }
 #pragma unroll
@@ -601,14 +603,14 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
 #pragma unroll
         for (int o = HREG / 2; o > 0; o >>= 1) {
             Sd += __shfl_xor_sync(0xffffffffu, Sd, o);
-            Kx += __shfl_xor_sync(0xffffffffu, Kx, o);
+            Kxd += __shfl_xor_sync(0xffffffffu, Kxd, o);
         }
         if (pub_lane) {
             Partial pr;
             pr.m = msl;                                   // raw units (the tail scales exponents)
             pr.amax = GREEDY ? ax : 0;
             pr.S = Sd;
-            pr.Kl = (double)Kx * (double)sc;
+            pr.Kl = Kxd * (double)sc;
             p.partials[idx] = pr;
         }
 #if MSD_PUB_LATE
@@ -714,16 +716,16 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                             const float2 e23 = __fadd2_rn(make_float2(e[4], e[5]), make_float2(e[6], e[7]));
                             s2[l] = __fadd2_rn(s2[l], __fadd2_rn(e01, e23));
                             if (l > 0) {
-                                // KL numerator sum e_l (z_l - z_{l-1}): the raw logit difference
-                                // (y_l - y_{l-1}) + (m_l - m_{l-1}) is exact in fp32, so the
-                                // O(1) cancellation against the normaliser difference happens
-                                // later in fp64 (R18)
+                                // KL numerator sum e_l (z_l - z_{l-1}) = sum e_l (y_l - y_{l-1}) +
+                                // (m_l - m_{l-1}) sum e_l: the centred differences y_l - y_{l-1}
+                                // (exact in fp32) are accumulated here, the offset term is added
+                                // by the publisher in float64 -- a constant logit offset between
+                                // the levels never enters the fp32 sums (R18)
                                 const float2 neg1 = make_float2(-1.f, -1.f);
-                                const float2 cm = make_float2(wm[l] - wm[l - 1], wm[l] - wm[l - 1]);
-                                float2 ka = __fmul2_rn(make_float2(e[0], e[1]), __fadd2_rn(__ffma2_rn(yprev[0], neg1, y[0]), cm));
-                                float2 kb = __fmul2_rn(make_float2(e[2], e[3]), __fadd2_rn(__ffma2_rn(yprev[1], neg1, y[1]), cm));
-                                ka = __ffma2_rn(make_float2(e[4], e[5]), __fadd2_rn(__ffma2_rn(yprev[2], neg1, y[2]), cm), ka);
-                                kb = __ffma2_rn(make_float2(e[6], e[7]), __fadd2_rn(__ffma2_rn(yprev[3], neg1, y[3]), cm), kb);
+                                float2 ka = __fmul2_rn(make_float2(e[0], e[1]), __ffma2_rn(yprev[0], neg1, y[0]));
+                                float2 kb = __fmul2_rn(make_float2(e[2], e[3]), __ffma2_rn(yprev[1], neg1, y[1]));
+                                ka = __ffma2_rn(make_float2(e[4], e[5]), __ffma2_rn(yprev[2], neg1, y[2]), ka);
+                                kb = __ffma2_rn(make_float2(e[6], e[7]), __ffma2_rn(yprev[3], neg1, y[3]), kb);
                                 k2[l] = __fadd2_rn(k2[l], __fadd2_rn(ka, kb));
                             }
 #pragma unroll
