@@ -50,7 +50,10 @@
 namespace msd {
 
 constexpr int NCW = 8;                 // pass-1 warps = element regions of an item
-constexpr int NCW2 = 8;                // pass-2 warps: warp v handles regions v, v + NCW2, ...
+#ifndef MSD_P2W
+#define MSD_P2W 8
+#endif
+constexpr int NCW2 = MSD_P2W;          // pass-2 warps: warp v handles regions v, v + NCW2, ...
 constexpr int NPR = NCW / NCW2;        // regions per pass-2 warp
 constexpr int CET = 32;                // elements per pass-1 thread per row
 constexpr int WCH = CET * 32;          // contiguous entries per region (1024)
@@ -106,7 +109,7 @@ struct Ctl {
     alignas(16) float r1K[R1][L][NW1][NSUB1];  // pass-1 KL numerators sum e (z_l - z_{l-1})
     int r1A[R1][L][NW1];                    // greedy: first argmax index per warp
     WF rowf[NQ][L][NW1];
-    float r2R[R2][L][NCW2][NSUB];           // pass-2 residual partials (probability units)
+    float r2R[R2][L][NCW][NSUB];            // pass-2 residual partials per region (probability units)
     unsigned long long fbuf_pad;
     unsigned long long fbuf[NFETCH][FBUF];  // fetcher staging of a unit's records
 };
@@ -846,13 +849,18 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         }
     } else if (warp >= W_P2) {
         // ================================================================ pass-2 warps
-        // warp W_P2 + v handles region v (same TMEM lane quadrant as pass-1 warp v)
-        static_assert(NPR == 1, "one region per pass-2 warp");
-        const int v = warp - W_P2;
-        if ((amask >> v) & 1u) {
+        // warp W_P2 + vw handles regions vw, vw + NCW2, ... (the same TMEM lane quadrant as
+        // pass-1 warp vw: NCW2 is a multiple of 4), one after the other for every item
+        const int vw = warp - W_P2;
+        uint32_t mine = 0;
+        for (int rr = 0; rr < NPR; ++rr) mine |= amask & (1u << (vw + NCW2 * rr));
+        if (mine) {
             PROF_DECL
             Cursor cu;
             for (; cu.j < n_my; cu.next(S, PP, PT, NT)) {
+              for (int rr = 0; rr < NPR; ++rr) {
+                const int v = vw + NCW2 * rr;
+                if (!((amask >> v) & 1u)) continue;
                 const int j = cu.j;
                 const bool isT = cu.isT(PT);
                 const int q = cu.q;
@@ -974,6 +982,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                 if (lane == 0) mbar_arrive(&c.r2_full[r2]);
                 PROF(4)
                 PROF_ITEM
+              }   // regions of this warp
             }
             PROF_FLUSH(1)
         }
@@ -1208,7 +1217,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         // ================================================================ reducer (slice residual)
         PROF_DECL
         // lane = 4 v + t: region v (half v / HREG), sub-record t; each half's 16 lanes fold
-        static_assert(NCW2 * NSUB == 32 && HREG * NSUB == 16, "reducer lane layout");
+        static_assert(NCW * NSUB == 32 && HREG * NSUB == 16, "reducer lane layout");
         const int v = lane >> 2, t = lane & 3;
         const bool act = (amask >> v) & 1u;
         const int tslice = NH * s + v / HREG;
