@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             for (int k = 0; k < NQ; ++k) {
                 mbar_init(&c.rowf_full[k], 1);
                 mbar_init(&c.rowf_empty[k], np2);
-                mbar_init(&c.pub[k], 1);
+                mbar_init(&c.pub[k], LSE ? (uint32_t)(nact * NSPLIT) : 1u);
             }
             for (int q = 0; q < NT; ++q) { mbar_init(&c.tm_full[q], nact * NSPLIT); mbar_init(&c.tm_empty[q], np2); }
             fence_mbar_init();
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         __syncwarp();
         if (lane == 0) {
             stamp(j, 5);
-            mbar_arrive(&c.pub[k]);
+            if (!LSE) mbar_arrive(&c.pub[k]);
         }
 #endif
         // then the tail's Partial, off the exchange's critical path: the slice sum again in
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
         __syncwarp();
         if (lane == 0) {
             stamp(j, 5);
-            mbar_arrive(&c.pub[k]);
+            if (!LSE) mbar_arrive(&c.pub[k]);
         }
 #endif
     };
@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                     const uint32_t bit = 1u << wi;
                     if (fast) atomicAnd(&c.clampw[k], ~bit);
                     else atomicOr(&c.clampw[k], bit);
+                    if (LSE && !p1only) mbar_arrive(&c.pub[k]);     // this warp's maxima are out
                 }
                 PROF(3)
                 if (lane < NSUB1) {
@@ -1076,6 +1077,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
             if (LSE && lane < L) lz = __ldg(p.lse + ((size_t)lane * p.B + b) * p.K + i);
             // the other slices of the unit are published around the time this one is: poll only
             // from then on (polls steal issue slots and L2 bandwidth)
+            // (LSE: pub[k] is arrived by the pass-1 warps themselves -- only their maxima are needed)
             mbar_wait_lat(&c.pub[k], (uint32_t)((j / NQ) & 1));
             const uint64_t t0 = globaltimer();
             PROF(4)
@@ -1125,7 +1127,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1) core_kernel(CoreParams p) {
                         if ((amask >> (w % NCW)) & 1u) mr = fmaxf(mr, c.wmx[k][lane][w]);
                 if (!(mr > NEG_MASKED)) mr = (float)(lz / (double)sc);
                 const double x = (double)mr * (double)sc - lz;       // <= 0 up to the rounding of mr
-                const float sn = lane < L ? (x <= 0.0 ? (float)(1.0 / dexp_neg(x)) : (float)dexp_neg(-x)) : 0.f;
+                // exp(-x) for -x >= 0 (dexp_neg's reduction holds for arguments up to ~700 either sign)
+                const float sn = lane < L ? (float)dexp_neg(-x) : 0.f;
 #pragma unroll
                 for (int l = 0; l < L; ++l) {
                     Rl[l] = __shfl_sync(0xffffffffu, mr, l);
