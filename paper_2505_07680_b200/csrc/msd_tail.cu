@@ -594,12 +594,33 @@ __device__ int32_t scan_slice(bool resid, const Tin* ra, const Tin* rb, double A
         }
         // within the margin of a token boundary: the float64 rescan below decides
     }
-    // (weights recomputed on demand: this path is rare and registers are not)
     ExpShift ea, eb;
     ea.init(sizeof(Tin) == 2 ? sh.exptab : nullptr, A);
     eb.init(sizeof(Tin) == 2 ? sh.exptab : nullptr, B);
-    const int best = scan_find([&](int k) { return wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, ea, eb); }, e0,
-                               before, target, sh, &found, &cprev_f, &c_f);
+    int best;
+    if (ea.tab && (!resid || eb.tab)) {
+        // table path: every gather of the thread's ET weights issued before any is used (one L2
+        // round trip), the float64 weights formed once (the two scans below reuse them)
+        double wd[ET];
+        exp_shift_batch<ET>(ea, xa, wd);
+        if (resid) {
+            double tb[ET];
+            exp_shift_batch<ET>(eb, xb, tb);
+#pragma unroll
+            for (int k = 0; k < ET; ++k) {
+                const double r = (xa[k] > NEG_MASKED ? wd[k] : 0.0) - (xb[k] > NEG_MASKED ? tb[k] : 0.0);
+                wd[k] = xa[k] > NEG_MASKED && r > 0.0 ? r : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < ET; ++k) wd[k] = xa[k] > NEG_MASKED ? wd[k] : 0.0;
+        }
+        best = scan_find([&](int k) { return wd[k]; }, e0, before, target, sh, &found, &cprev_f, &c_f);
+    } else {
+        // (weights recomputed on demand: no table -- f32 logits or a temperature)
+        best = scan_find([&](int k) { return wt(resid, xa[k], resid ? xb[k] : NEG_CLAMP, ea, eb); }, e0,
+                         before, target, sh, &found, &cprev_f, &c_f);
+    }
     if (best != 0x7fffffff && found == best) {
         *tie = fabs(u - cprev_f / Z) < TIE_EPS || fabs(u - c_f / Z) < TIE_EPS;
         sh.near = *tie ? 1 : 0;
