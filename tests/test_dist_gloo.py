@@ -79,7 +79,9 @@ def _worker(rank, world, port, q):
         mdist.allreduce_stats(pool)
         boot = mdist.ChainScheduler(T_ms=[1.0, 3.0, 10.0], W=K)
         bchain = boot.bootstrap(pool.tolist())
-        q.put((r, req0, b, stats.numpy().copy(), chain, sch.t_eff, [t[:, :, :8].clone() for t in inp.levels],
+        # numpy copies only: torch tensors would travel as shared-memory handles, which the parent
+        # cannot open once this process has exited
+        q.put((r, req0, b, stats.numpy().copy(), chain, sch.t_eff, [t[:, :, :8].numpy().copy() for t in inp.levels],
                pool.numpy().copy(), bchain, boot.sim))
         dist.barrier()
         dist.destroy_process_group()
@@ -119,7 +121,7 @@ def test_sharded_inputs_equal_unsharded(two_ranks):
     full = _inputs(2 * B_LOCAL, 0)
     for r, req0, b, _, _, _, lv in (o[:7] for o in two_ranks):
         for l in range(L):
-            assert torch.equal(lv[l], full.levels[l][req0:req0 + b, :, :8])
+            assert np.array_equal(lv[l], full.levels[l][req0:req0 + b, :, :8].numpy())
 
 
 def test_allreduced_stats_identical_and_exact(two_ranks):
