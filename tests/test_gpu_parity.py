@@ -147,6 +147,19 @@ def test_full_llama3_batch_sampled_requests():
     assert not (f & api.FLAG["TIMEOUT"]).any()
 
 
+@pytest.mark.parametrize("name", ["qwen25", "llama2", "sweep"])
+def test_full_batch_sampled_requests_other_configs(name):
+    # the other BASELINE configurations at their full sizes in one call (Qwen B=256 V=151936 K=6;
+    # Llama-2 B=64 V=32000 K=5; the 4-level sweep pool V=128256): sampled requests vs the oracle
+    inp = _gauss(name)
+    o = _run(inp)
+    B = inp.B
+    req = sorted({0, B // 7, B // 3, B // 2, (2 * B) // 3, B - 1})
+    ref = run_oracle(inp, requests=req)
+    assert_parity(o, ref, requests=req)
+    assert not (to_np(o)["flags"] & api.FLAG["TIMEOUT"]).any()
+
+
 def test_deterministic_bit_identical():
     inp = _gauss("qwen25", B=12, V=70000)
     a = {k: v.clone() for k, v in _run(inp).items()}
